@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Bench: candidate schedules rounded + evaluated per second (BASELINE.json metric).
+
+A step = one pass of the whole hot path (a1-a7 of SURVEY §8(a), plus the a8 NCCL
+MIN all-reduce at N>1) over one batch of synthetic, device-resident S*.
+Default workload: the ResNet-50-shaped training DAG (n=353, |E|=560), G1 LP-like S*,
+theta = 0.5, 16 budgets, 125,000 S* per GPU per step (the 10^6-candidate config
+sharded over 8 GPUs; weak scaling).  Inputs (31 GB per GPU) exceed L2 (126 MB), so no
+flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate schedules rounded+evaluated/sec at n≈350, 1/2/4/8 B200; % HBM roofline"
+UNIT = "candidates/s"
+
+CONFIGS = {
+    # name: (graph builder, family, thetas, budget rule, S* per GPU per step)
+    "resnet50": ("resnet50", "g1", [0.5], "grid16", 125000),
+    "vgg16": ("vgg16", "g1", [0.5], "grid16", 100000),
+    "unet": ("unet", "g1", [0.5], "unet", 125000),
+    "mobilenet": ("mobilenet", "g1", [0.5], "grid16", 125000),
+    "fcn8": ("fcn8", "g1", [0.5], "grid16", 62500),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
+    ap.add_argument("--family", default=None)
+    ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
+    ap.add_argument("--layout", default="tri4", choices=["tri4", "dense"])
+    ap.add_argument("--e2e-batch", type=int, default=16384)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def build_workload(cfg, family=None):
+    from workloads import budgets as B
+    from workloads import graphs as G
+    gname, fam, thetas, rule, batch = CONFIGS[cfg]
+    g = G.NETWORKS[gname]()
+    if rule == "unet":
+        budgets = B.unet_grid(g)
+        g = g.scaled(5)
+    else:
+        budgets = B.geometric_grid(g, 16)
+    return g, (family or fam), thetas, budgets, batch
+
+
+def tri_bytes(n):
+    return 4 * n * (n - 1) // 2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(cfg):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(cfg)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons DURING the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+
+def _oracle_worker(args):
+    gname, fam, seed, s_list, thetas, cfg = args
+    from oracle import Instance, evaluate
+    from workloads.sstar import gen_sstar
+    g, _, _, _, _ = build_workload(cfg, fam)
+    inst = Instance.from_graph(g)
+    xs = [gen_sstar(g, fam, seed, s, 1)[0] for s in s_list]
+    t0 = time.perf_counter()
+    for x in xs:
+        for th in thetas:
+            evaluate(inst, x, th)
+    return time.perf_counter() - t0, len(xs) * len(thetas)
+
+
+def cpu_oracle_rate(cfg, fam, seed, thetas, seconds):
+    """The oracle as it stands on this host's cores (multiprocessing), bounded sample."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    # calibrate one candidate on one core
+    dt, cnt = _oracle_worker((None, fam, seed, [0], thetas, cfg))
+    per = dt / cnt
+    per_core = max(1, int(seconds / per / len(thetas)))
+    jobs = [(None, fam, seed, list(range(1 + c * per_core, 1 + (c + 1) * per_core)), thetas, cfg)
+            for c in range(cores)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_oracle_worker, jobs)
+    wall = time.perf_counter() - t0
+    total = sum(r[1] for r in res)
+    busy = max(r[0] for r in res)
+    return {"value": total / busy, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{total} candidates (S* #1..{cores * per_core}, {fam}, theta={thetas}) of the "
+                      f"{cfg} workload on {cores} processes; {wall:.1f}s wall incl. pool start"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    g, fam, thetas, budgets, batch = build_workload(a.config, a.family)
+    from oracle import Instance, evaluate
+    from workloads.sstar import gen_sstar
+    inst = Instance.from_graph(g)
+    cores = len(os.sched_getaffinity(0))
+    per_step = 8
+    xs = [gen_sstar(g, fam, 7, s, 1)[0] for s in range(per_step)]
+    for _ in range(a.warmup):
+        evaluate(inst, xs[0], thetas[0])
+    t0 = time.perf_counter()
+    cnt = 0
+    for _ in range(a.steps):
+        for x in xs:
+            for th in thetas:
+                evaluate(inst, x, th)
+                cnt += 1
+    dt = time.perf_counter() - t0
+    v = cnt / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1000 * dt / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{a.config} n={g.n} |E|={len(g.edges)} {fam} S*, theta={thetas}, "
+                                   f"{len(budgets)} budgets", "global_batch": per_step * len(thetas)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} S* x {len(thetas)} theta per step, 1 process"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    del cores
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_02653_b200 as cm
+    from paper_1910_02653_b200.dist import global_best
+    from workloads.device_gen import DeviceGenerator
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    g, fam, thetas, budgets, batch = build_workload(a.config, a.family)
+    if a.batch:
+        batch = a.batch
+    seed = 20250101
+    n_theta = len(thetas)
+    graph = cm.Graph.from_workload(g)
+    gen = DeviceGenerator(g, fam, seed, layout=a.layout)
+    sstar = torch.empty(gen.shape(batch), dtype=torch.float32, device=dev)
+    s_base = rank * batch
+    gen.fill(sstar, s_base)
+    th = torch.tensor(thetas, dtype=torch.float32, device=dev)
+    bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
+    key = torch.empty(len(budgets), dtype=torch.int64, device=dev)
+    peak = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
+    cost = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
+    total = world * batch * n_theta
+    stream = torch.cuda.current_stream(dev)
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+
+    def step(i=None):
+        key.fill_(cm.CM_KEY_NONE)
+        if i is not None:
+            k_start[i].record(stream)
+        cm.round_and_evaluate(graph, sstar, th, bu, layout=a.layout, index_base=s_base * n_theta,
+                              total_candidates=total, best_key=key, peak=peak, cost=cost,
+                              stream=stream.cuda_stream)
+        if i is not None:
+            k_end[i].record(stream)
+        global_best(key)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0.record(stream)
+    for i in range(a.steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    elapsed_ms = t0.elapsed_time(t1)
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(k_start, k_end)]))
+    if world > 1:
+        t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kern_ms = float(t[0]), float(t[1])
+    best = key.cpu().tolist()
+
+    # ---- e2e through the public API with HOST buffers (rank-local, then the same MIN) ----
+    e2e = None
+    if not a.no_e2e:
+        eb = min(a.e2e_batch, batch)
+        host = torch.empty((eb, gen.stride), dtype=torch.float32, pin_memory=True)
+        host.copy_(sstar.view(batch, -1)[:eb])
+        pipe = cm.HostPipeline(graph, gen.stride, chunk=2048, n_theta=n_theta, n_budget=len(budgets),
+                               layout=a.layout, ld=gen.ld if a.layout == "dense" else None, device=dev)
+        pipe.run(host, th, bu, index_base=s_base * n_theta, total_candidates=world * eb * n_theta)
+        torch.cuda.synchronize()
+        e_steps = max(1, min(a.steps, 5))
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(e_steps):
+            _, _, kk = pipe.run(host, th, bu, index_base=rank * eb * n_theta,
+                                total_candidates=world * eb * n_theta)
+            if world > 1:
+                kd = kk.to(dev)
+                global_best(kd)
+                kk = kd.cpu()
+        e_dt = time.perf_counter() - te
+        if world > 1:
+            t = torch.tensor([e_dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_dt = float(t[0])
+        e2e = {"value": world * eb * n_theta * e_steps / e_dt, "unit": UNIT,
+               "h2d_bytes_per_step": eb * gen.stride * 4,
+               "d2h_bytes_per_step": eb * n_theta * 16 + 8 * len(budgets),
+               "batch_per_gpu": eb, "host_memory": "pinned"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    cand_per_step = world * batch * n_theta
+    value = cand_per_step * a.steps / (elapsed_ms / 1000.0)
+    peak_gbs, peak_src = load_peaks()
+    alg_bytes = batch * tri_bytes(g.n) + batch * n_theta * 16 + 8 * len(budgets)
+    achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
+    traffic = load_traffic(a.config)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+            "frac": achieved / peak_gbs, "traffic": traffic,
+            "kernel": "cmk::round_evaluate_kernel", "kernel_ms": kern_ms,
+            "alg_bytes_per_launch": alg_bytes, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    cpu = None
+    if not a.no_cpu_baseline and world == 1:
+        cpu = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": elapsed_ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"{a.config}: n={g.n}, |E|={len(g.edges)}, {fam} LP-like S* "
+                                   f"({a.layout} fp32), theta={thetas}, {len(budgets)} budgets",
+                       "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
+                       "parallelism": f"candidates sharded over {world} GPU(s), NCCL MIN all-reduce of keys",
+                       "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush"},
+            "gpu_launches": a.steps, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks,
+            "best": [cm.decode_key(k, cm.key_idx_bits(total)) for k in best]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,116 @@
+/*
+ * cm.h -- C ABI of the B200 (sm_100a) Checkmate two-phase-rounding hot path.
+ *
+ * Checkmate (Jain et al., MLSys 2020, arXiv:1910.02653), §5.2 Alg. 2
+ * "Two-phase rounding" plus the memory accounting of §4.4
+ * Eqs. 6-9.  For every candidate (S*, theta) the library
+ *   a1  rounds   S_{t,i} = 1[S*_{t,i} > theta], i < t            (Eq. 12b)
+ *   a2  seeds    R_t <- e_t | (S_{t+1} & ~S_t)                   (Alg. 2 lines 2-5)
+ *   a3  closes   R_{t,i} <- 1 while R_{t,j} > R_{t,i} + S_{t,i}   (Alg. 2 lines 6-8)
+ *   a4  frees    FREE_{t,i,k} per Eq. 9
+ *   a5  peaks    peak = max_{t,k} U_{t,k}, Eqs. 6-8
+ *   a6  scores   cost = sum_t sum_i C_i R_{t,i}                  (objective (1))
+ *   a7  reduces  per budget b: min over {c : peak_c <= b} of (cost_c, idx_c)  (budget row PAPER.md:311)
+ * Semantics (tie rule, horizon, units) are fixed in DESIGN.md "Readings".
+ *
+ * Index conventions: node v_i <-> 0-based i-1; stage t <-> row t-1.  All
+ * integers are int64 (C in ns, M in bytes); results are bit-exact.
+ *
+ * Ownership: every pointer is caller-owned; the library never frees caller
+ * memory.  A cm_graph owns a device-resident copy of the graph.
+ * Errors: validation errors are returned before any launch; CUDA failures
+ * (including asynchronous faults surfacing at the next call) return
+ * CM_ECUDA.  Nothing throws across the ABI.  cm_last_error() gives a
+ * thread-local human-readable detail string for the last non-OK status.
+ */
+#ifndef CHECKMATE_B200_CM_H
+#define CHECKMATE_B200_CM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CM_OK = 0,
+  CM_EINVAL = 1,  /* NULL pointer, n < 1, bad ld / stride / layout / alignment, counts < 0 */
+  CM_ETOPO = 2,   /* edge (i, j) with i >= j: nodes must be topologically numbered */
+  CM_EDUP = 3,    /* duplicate edge: E is a set */
+  CM_ERANGE = 4,  /* n > CM_NMAX, |E| > CM_EMAX, shared memory exceeded, or an int64 bound overflows */
+  CM_ECUDA = 5,   /* CUDA error (incl. asynchronous faults from an earlier launch) */
+  CM_ENOMEM = 6   /* device allocation failed */
+} cm_status;
+
+#define CM_NMAX 1024          /* max nodes (stages T = n) */
+#define CM_EMAX 8192          /* max edges */
+#define CM_LAYOUT_DENSE 0     /* S* row r at sstar + r*ld, ld >= n, ld % 4 == 0 */
+#define CM_LAYOUT_TRI4 1      /* S* row r at sstar + sum_{r'<r} roundup4(r') (packed strict lower triangle) */
+#define CM_KEY_NONE INT64_MAX /* best_key value meaning "no feasible candidate" */
+
+/* cudaStream_t without pulling in CUDA headers (same type: struct CUstream_st*). NULL = legacy stream. */
+typedef struct CUstream_st* cm_stream;
+
+typedef struct cm_graph cm_graph; /* opaque, immutable after create, device-resident, thread-safe to share */
+
+/*
+ * cm_graph_create -- validate a DAG G=(V,E) with C, M and
+ * upload it to the CURRENT CUDA device.
+ *   n              node count, 1 <= n <= CM_NMAX
+ *   pred_ptr       host int32[n+1], CSR offsets of DEPS(k) = {i : (i,k) in E};
+ *                  pred_ptr[0] == 0, non-decreasing, pred_ptr[n] = |E| <= CM_EMAX
+ *   pred_idx       host int32[|E|], 0-based predecessors; every i < k (CM_ETOPO), no repeats (CM_EDUP)
+ *   cost, mem      host int64[n], C_i >= 0 (ns), M_i >= 0 (bytes)
+ *   mem_overhead   M_input + 2 M_param >= 0, the Eq. 6 constant
+ *   out            receives the handle
+ * Checks ovh + sum M < 2^62 and sum_i (n-i) C_i < 2^62 (CM_ERANGE).  Builds the
+ * successor CSR USERS(i) itself.  Host pointers are only read.
+ */
+cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pred_idx,
+                          const int64_t* cost, const int64_t* mem, int64_t mem_overhead,
+                          cm_graph** out);
+void cm_graph_destroy(cm_graph* g);          /* NULL is a no-op; call after work using g completed */
+int32_t cm_graph_n(const cm_graph* g);
+int64_t cm_graph_cost_bound(const cm_graph* g); /* sum_i (n-i) C_i: an upper bound of every cost */
+
+typedef struct {
+  int32_t n_sstar;          /* number of S* matrices in this call, >= 0 */
+  int32_t layout;           /* CM_LAYOUT_DENSE or CM_LAYOUT_TRI4 */
+  const float* sstar;       /* device, 16-byte aligned; only entries i < t of row t are read (Eq. 12b) */
+  int64_t ld;               /* dense: row stride in floats, ld >= n, ld % 4 == 0; tri4: ignored */
+  int64_t sstar_stride;     /* floats between consecutive S*, % 4 == 0; >= n*ld (dense) / tri4 size */
+  int32_t n_theta;          /* >= 1 */
+  const float* theta;       /* device fp32[n_theta]; rule S = S* > theta, NaN -> 0 (Q1, Q6) */
+  int32_t n_budget;         /* >= 0 */
+  const int64_t* budget;    /* device int64[n_budget]; feasible iff peak <= budget (Q7) */
+  int64_t index_base;       /* global idx of candidate (s, j) = index_base + s*n_theta + j */
+  int64_t total_candidates; /* global candidate count (all ranks); sizes the key's index field */
+  int64_t* peak;            /* device int64[n_sstar*n_theta], required */
+  int64_t* cost;            /* device int64[n_sstar*n_theta], required */
+  int64_t* best_key;        /* device int64[n_budget] (may be NULL iff n_budget == 0); in/out:
+                               atomicMin of (cost << idx_bits | idx) into caller-initialised values
+                               (CM_KEY_NONE = nothing feasible yet) */
+  uint64_t* r_mask;         /* device [n_cand][n][W], W = ceil(n/64), or NULL: R rows, bit i%64 of word i/64 */
+  uint64_t* s_mask;         /* device [n_cand][n][W] or NULL: S rows */
+} cm_eval_args;
+
+/*
+ * cm_round_and_evaluate -- a1..a7 for every (S*, theta) candidate of one batch.
+ * Stream-ordered and asynchronous on `stream`: no host synchronisation, no
+ * allocation.  CM_ERANGE if total_candidates needs so many index bits that the
+ * cost bound no longer fits the key (cost_bound >= 2^(63 - idx_bits)).
+ */
+cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* args, cm_stream stream);
+
+/* idx_bits used by the key packing: number of bits of (total_candidates - 1); 0 when total <= 1. */
+int32_t cm_key_idx_bits(int64_t total_candidates);
+/* key -> (cost, idx); key == CM_KEY_NONE -> cost = -1, idx = -1. */
+void cm_decode_key(int64_t key, int32_t idx_bits, int64_t* cost, int64_t* idx);
+
+const char* cm_status_string(cm_status s);
+const char* cm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHECKMATE_B200_CM_H */

@@ -1,0 +1,228 @@
+"""B200 (sm_100a) hot path of Checkmate two-phase rounding (arXiv:1910.02653).
+
+Thin Python binding over the C ABI of include/cm.h -- argument marshalling only;
+every step of the path (rounding, R closure, FREE, U peak, cost, per-budget
+argmin) runs in libcheckmate_b200.so.  PyTorch supplies device memory and
+streams.  Importing fails loudly when the shared library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _abi
+from ._abi import (CM_EMAX, CM_KEY_NONE, CM_LAYOUT_DENSE, CM_LAYOUT_TRI4,  # noqa: F401
+                   CM_NMAX)
+
+_lib = _abi.load()
+
+
+class CMError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.cm_status_string(status).decode()
+        detail = _lib.cm_last_error().decode()
+        super().__init__(f"{where}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def _check(status: int, where: str):
+    if status != _abi.CM_OK:
+        raise CMError(status, where)
+
+
+def tri4_size(n: int) -> int:
+    q, m = divmod(n, 4)
+    return 8 * q * (q - 1) + 12 * q + (4 * q if m > 0 else 0) + max(m - 1, 0) * (4 * q + 4)
+
+
+class Graph:
+    """Device-resident DAG (cm_graph).  pred_ptr/pred_idx: CSR of DEPS(k), 0-based."""
+
+    def __init__(self, n, pred_ptr, pred_idx, cost, mem, ovh):
+        self.n = int(n)
+        pp = np.ascontiguousarray(pred_ptr, np.int32)
+        pi = np.ascontiguousarray(pred_idx, np.int32)
+        c = np.ascontiguousarray(cost, np.int64)
+        m = np.ascontiguousarray(mem, np.int64)
+        h = ctypes.c_void_p()
+        st = _lib.cm_graph_create(self.n, pp.ctypes.data, pi.ctypes.data if pi.size else None,
+                                  c.ctypes.data, m.ctypes.data, int(ovh), ctypes.byref(h))
+        _check(st, "cm_graph_create")
+        self._h = h
+        self.cost_bound = int(_lib.cm_graph_cost_bound(h))
+
+    @classmethod
+    def from_edges(cls, n, edges, cost, mem, ovh):
+        ptr = np.zeros(n + 1, np.int32)
+        for (_, j) in edges:
+            ptr[j + 1] += 1
+        ptr = np.cumsum(ptr).astype(np.int32)
+        idx = np.zeros(len(edges), np.int32)
+        fill = ptr[:-1].copy()
+        for (i, j) in sorted(edges, key=lambda e: (e[1], e[0])):
+            idx[fill[j]] = i
+            fill[j] += 1
+        return cls(n, ptr, idx, cost, mem, ovh)
+
+    @classmethod
+    def from_workload(cls, g):
+        return cls.from_edges(g.n, g.edges, g.cost, g.mem, g.ovh)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.cm_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def key_idx_bits(total_candidates: int) -> int:
+    return int(_lib.cm_key_idx_bits(int(total_candidates)))
+
+
+def decode_key(key: int, idx_bits: int):
+    c = ctypes.c_int64()
+    i = ctypes.c_int64()
+    _lib.cm_decode_key(int(key), int(idx_bits), ctypes.byref(c), ctypes.byref(i))
+    return int(c.value), int(i.value)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str = "dense",
+                       n_sstar: int | None = None, ld: int | None = None, stride: int | None = None,
+                       index_base: int = 0, total_candidates: int | None = None,
+                       best_key=None, masks: bool = False, peak=None, cost=None, stream=None):
+    """cm_round_and_evaluate on device tensors.
+
+    sstar : float32 CUDA tensor; dense [N_S, n, ld] or tri4 [N_S, tri4_size(n)] (or any
+            buffer with explicit n_sstar / ld / stride).
+    theta : float32 CUDA tensor [N_theta];  budget: int64 CUDA tensor [N_B] or None.
+    Returns dict(peak, cost, best_key, idx_bits, r_mask, s_mask) of CUDA tensors.
+    Asynchronous on ``stream`` (default: torch's current stream).
+    """
+    import torch
+    n = graph.n
+    lay = {"dense": CM_LAYOUT_DENSE, "tri4": CM_LAYOUT_TRI4}[layout]
+    if n_sstar is None:
+        n_sstar = sstar.shape[0]
+    if lay == CM_LAYOUT_DENSE:
+        if ld is None:
+            ld = sstar.shape[-1]
+        if stride is None:
+            stride = n * ld if sstar.dim() < 3 else sstar.stride(0)
+    else:
+        ld = 0
+        if stride is None:
+            stride = sstar.stride(0) if sstar.dim() == 2 else tri4_size(n)
+    dev = sstar.device
+    n_theta = theta.numel()
+    n_cand = n_sstar * n_theta
+    n_budget = 0 if budget is None else budget.numel()
+    if total_candidates is None:
+        total_candidates = index_base + n_cand
+    if peak is None:
+        peak = torch.empty(n_cand, dtype=torch.int64, device=dev)
+    if cost is None:
+        cost = torch.empty(n_cand, dtype=torch.int64, device=dev)
+    if best_key is None and n_budget:
+        best_key = torch.full((n_budget,), CM_KEY_NONE, dtype=torch.int64, device=dev)
+    r_mask = s_mask = None
+    if masks:
+        W = (n + 63) // 64
+        r_mask = torch.zeros((n_cand, n, W), dtype=torch.int64, device=dev)
+        s_mask = torch.zeros((n_cand, n, W), dtype=torch.int64, device=dev)
+    a = _abi.EvalArgs()
+    a.n_sstar = n_sstar
+    a.layout = lay
+    a.sstar = sstar.data_ptr()
+    a.ld = int(ld)
+    a.sstar_stride = int(stride)
+    a.n_theta = n_theta
+    a.theta = theta.data_ptr()
+    a.n_budget = n_budget
+    a.budget = _ptr(budget)
+    a.index_base = int(index_base)
+    a.total_candidates = int(total_candidates)
+    a.peak = peak.data_ptr()
+    a.cost = cost.data_ptr()
+    a.best_key = _ptr(best_key)
+    a.r_mask = _ptr(r_mask)
+    a.s_mask = _ptr(s_mask)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(_lib.cm_round_and_evaluate(graph.handle, ctypes.byref(a), ctypes.c_void_p(stream)),
+           "cm_round_and_evaluate")
+    return {"peak": peak, "cost": cost, "best_key": best_key,
+            "idx_bits": key_idx_bits(total_candidates), "r_mask": r_mask, "s_mask": s_mask}
+
+
+class HostPipeline:
+    """End-to-end path for S* batches in (pinned) HOST memory.
+
+    The batch is cut into chunks; chunk c is copied host->device on a copy stream into
+    one of two device buffers while the kernel evaluates chunk c-1 on the compute stream
+    (double buffering with CUDA events), then peak / cost / keys come back device->host.
+    Device buffers are allocated once here, not per call."""
+
+    def __init__(self, graph: Graph, row_floats: int, chunk: int, n_theta: int, n_budget: int,
+                 layout: str = "tri4", ld: int | None = None, device="cuda"):
+        import torch
+        self.graph, self.chunk, self.layout = graph, int(chunk), layout
+        self.ld, self.row_floats = ld, int(row_floats)
+        self.dev = torch.device(device)
+        self.bufs = [torch.empty((self.chunk, self.row_floats), dtype=torch.float32, device=self.dev)
+                     for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.compute_stream = torch.cuda.Stream(self.dev)
+        self.n_theta, self.n_budget = n_theta, n_budget
+
+    def run(self, host_sstar, theta, budget=None, index_base: int = 0, total_candidates=None):
+        """host_sstar: pinned CPU float32 tensor [N_S, row_floats]; theta / budget: CUDA tensors.
+        Returns (peak, cost, best_key) as CPU tensors (synchronised)."""
+        import torch
+        N = host_sstar.shape[0]
+        n_cand = N * self.n_theta
+        total = index_base + n_cand if total_candidates is None else total_candidates
+        peak = torch.empty(n_cand, dtype=torch.int64, device=self.dev)
+        cost = torch.empty(n_cand, dtype=torch.int64, device=self.dev)
+        key = None
+        if budget is not None:
+            key = torch.full((budget.numel(),), CM_KEY_NONE, dtype=torch.int64, device=self.dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        freed = [torch.cuda.Event() for _ in range(2)]
+        cs, ks = self.copy_stream, self.compute_stream
+        ks.wait_stream(torch.cuda.current_stream(self.dev))
+        for c, s0 in enumerate(range(0, N, self.chunk)):
+            cnt = min(self.chunk, N - s0)
+            b = c & 1
+            buf = self.bufs[b]
+            with torch.cuda.stream(cs):
+                if c >= 2:
+                    cs.wait_event(freed[b])
+                buf[:cnt].copy_(host_sstar[s0:s0 + cnt], non_blocking=True)
+                copied[b].record(cs)
+            with torch.cuda.stream(ks):
+                ks.wait_event(copied[b])
+                lo, hi = s0 * self.n_theta, (s0 + cnt) * self.n_theta
+                round_and_evaluate(self.graph, buf, theta, budget, layout=self.layout, n_sstar=cnt,
+                                   ld=self.ld, stride=self.row_floats, index_base=index_base + lo,
+                                   total_candidates=total, best_key=key, peak=peak[lo:hi],
+                                   cost=cost[lo:hi], stream=ks.cuda_stream)
+                freed[b].record(ks)
+        with torch.cuda.stream(ks):
+            out = (peak.to("cpu", non_blocking=True), cost.to("cpu", non_blocking=True),
+                   None if key is None else key.to("cpu", non_blocking=True))
+        ks.synchronize()
+        return out

@@ -1,0 +1,72 @@
+"""ctypes declarations of include/cm.h (argument marshalling only).
+
+The shared library is built in-tree (paper_1910_02653_b200/build.py).  There is
+no fallback: if the library is missing or fails to load, importing the binding
+raises, so nothing can silently run on the CPU."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcheckmate_b200.so")
+
+CM_OK, CM_EINVAL, CM_ETOPO, CM_EDUP, CM_ERANGE, CM_ECUDA, CM_ENOMEM = range(7)
+CM_NMAX = 1024
+CM_EMAX = 8192
+CM_LAYOUT_DENSE = 0
+CM_LAYOUT_TRI4 = 1
+CM_KEY_NONE = (1 << 63) - 1
+
+EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
+           "cm_round_and_evaluate", "cm_key_idx_bits", "cm_decode_key", "cm_status_string",
+           "cm_last_error")
+
+
+class EvalArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_sstar", ctypes.c_int32),
+        ("layout", ctypes.c_int32),
+        ("sstar", ctypes.c_void_p),
+        ("ld", ctypes.c_int64),
+        ("sstar_stride", ctypes.c_int64),
+        ("n_theta", ctypes.c_int32),
+        ("theta", ctypes.c_void_p),
+        ("n_budget", ctypes.c_int32),
+        ("budget", ctypes.c_void_p),
+        ("index_base", ctypes.c_int64),
+        ("total_candidates", ctypes.c_int64),
+        ("peak", ctypes.c_void_p),
+        ("cost", ctypes.c_void_p),
+        ("best_key", ctypes.c_void_p),
+        ("r_mask", ctypes.c_void_p),
+        ("s_mask", ctypes.c_void_p),
+    ]
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_1910_02653_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    lib.cm_graph_create.argtypes = [ctypes.c_int32, P, P, P, P, ctypes.c_int64, ctypes.POINTER(P)]
+    lib.cm_graph_create.restype = ctypes.c_int
+    lib.cm_graph_destroy.argtypes = [P]
+    lib.cm_graph_destroy.restype = None
+    lib.cm_graph_n.argtypes = [P]
+    lib.cm_graph_n.restype = ctypes.c_int32
+    lib.cm_graph_cost_bound.argtypes = [P]
+    lib.cm_graph_cost_bound.restype = ctypes.c_int64
+    lib.cm_round_and_evaluate.argtypes = [P, ctypes.POINTER(EvalArgs), P]
+    lib.cm_round_and_evaluate.restype = ctypes.c_int
+    lib.cm_key_idx_bits.argtypes = [ctypes.c_int64]
+    lib.cm_key_idx_bits.restype = ctypes.c_int32
+    lib.cm_decode_key.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.POINTER(ctypes.c_int64)]
+    lib.cm_decode_key.restype = None
+    lib.cm_status_string.argtypes = [ctypes.c_int]
+    lib.cm_status_string.restype = ctypes.c_char_p
+    lib.cm_last_error.argtypes = []
+    lib.cm_last_error.restype = ctypes.c_char_p
+    return lib

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs.  Integer outputs must be bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import Instance, best_per_budget, evaluate, masks_u64
+from workloads import budgets as B
+from workloads import graphs as G
+from workloads.sstar import dense_to_tri4, from_binary, gen_sstar, roundup4
+
+pytestmark = pytest.mark.gpu
+
+KEY_NONE = (1 << 63) - 1
+
+
+def gpu_run(g, sstar, thetas, budgets=None, layout="dense", masks=False, index_base=0,
+            total=None, ld=None):
+    import torch
+    import paper_1910_02653_b200 as cm
+    dev = torch.device("cuda:0")
+    graph = cm.Graph.from_workload(g)
+    x = torch.from_numpy(np.ascontiguousarray(sstar)).to(dev)
+    th = torch.tensor(np.asarray(thetas, np.float32), device=dev)
+    bu = None if budgets is None else torch.tensor(np.asarray(budgets, np.int64), device=dev)
+    out = cm.round_and_evaluate(graph, x, th, bu, layout=layout, masks=masks, index_base=index_base,
+                                total_candidates=total, ld=ld)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+    graph.close()
+    return res
+
+
+def oracle_run(g, sstar_dense, thetas, keep=False):
+    inst = Instance.from_graph(g)
+    outs = []
+    for s in range(sstar_dense.shape[0]):
+        for th in thetas:
+            outs.append(evaluate(inst, sstar_dense[s], th, keep=keep))
+    return inst, outs
+
+
+def compare(g, sstar_dense, thetas, budgets=None, masks=False, layout="dense", index_base=0,
+            total=None):
+    src = sstar_dense if layout == "dense" else dense_to_tri4(sstar_dense)
+    res = gpu_run(g, src, thetas, budgets, layout=layout, masks=masks, index_base=index_base,
+                  total=total, ld=sstar_dense.shape[2] if layout == "dense" else None)
+    inst, outs = oracle_run(g, sstar_dense, thetas, keep=masks)
+    peaks = [o["peak"] for o in outs]
+    costs = [o["cost"] for o in outs]
+    assert list(res["peak"]) == peaks
+    assert list(res["cost"]) == costs
+    if masks:
+        for c, o in enumerate(outs):
+            assert np.array_equal(res["r_mask"][c].view(np.uint64), masks_u64(inst, o["R"])), c
+            assert np.array_equal(res["s_mask"][c].view(np.uint64), masks_u64(inst, o["S"])), c
+    if budgets is not None:
+        want = best_per_budget(peaks, costs, budgets, index_base)
+        bits = res["idx_bits"]
+        for b, key in enumerate(res["best_key"]):
+            if want[b][0] < 0:
+                assert key == KEY_NONE
+            else:
+                assert (int(key) >> bits, int(key) & ((1 << bits) - 1) if bits else 0) == \
+                    (want[b][1], want[b][0])
+    return res, outs
+
+
+def test_config1_path8():
+    """BASELINE config 1: path n=8, unit C/M, 64 S* x 4 thresholds x 3 budgets."""
+    g = G.path(8)
+    x = gen_sstar(g, "mix", 1, 0, 64)
+    compare(g, x, [0.3, 0.4, 0.5, 0.6], [2, 4, 8], masks=True)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13])
+@pytest.mark.parametrize("fam", ["g1", "g2"])
+def test_small_random(n, fam):
+    g = G.random_dag(n, 0.4, 10 + n)
+    x = gen_sstar(g, fam, 3, 0, 8)
+    compare(g, x, [0.5, 0.2], [g.ovh + 5, g.ovh + 20, 10 ** 9], masks=True)
+
+
+@pytest.mark.parametrize("n", [31, 32, 33, 63, 64, 65, 95, 96, 97, 127, 128, 129, 191, 257])
+def test_word_boundaries(n):
+    g = G.random_dag(n, 0.05, n)
+    x = gen_sstar(g, "g1" if n % 2 else "g2", 5, 0, 3)
+    compare(g, x, [0.5, 0.8], [B.p_floor(g), B.p_live(g)], masks=True)
+
+
+@pytest.mark.parametrize("L", [15, 16, 17, 31, 32, 33, 48])
+def test_training_random(L):
+    g = G.random_training(L, 0.05, L)
+    x = gen_sstar(g, "mix", 7, 0, 4)
+    compare(g, x, [0.5], B.geometric_grid(g, 5), masks=True)
+
+
+@pytest.mark.parametrize("name", ["vgg16", "resnet50", "unet", "mobilenet", "fcn8"])
+def test_paper_shaped(name):
+    g = G.NETWORKS[name]()
+    if name == "unet":
+        base = g
+        g = g.scaled(5)
+        budgets = B.unet_grid(base)
+    else:
+        budgets = B.geometric_grid(g, 16)
+    x = gen_sstar(g, "mix", 11, 100, 3)
+    compare(g, x, [0.5, 0.35], budgets, masks=(name == "resnet50"))
+
+
+def test_layouts_and_ld():
+    g = G.resnet50()
+    x = gen_sstar(g, "g1", 2, 0, 3)
+    r1, _ = compare(g, x, [0.5], layout="tri4")
+    wide = gen_sstar(g, "g1", 2, 0, 3, ld=roundup4(g.n) + 64, upper=np.nan)
+    r2, _ = compare(g, wide, [0.5])
+    assert np.array_equal(r1["peak"], r2["peak"]) and np.array_equal(r1["cost"], r2["cost"])
+
+
+def test_rounding_edge_values():
+    """Exact 0.5 ties, NaN, theta 0 and 1, garbage in the never-read upper triangle."""
+    g = G.random_training(10, 0.2, 4)
+    x = gen_sstar(g, "g2", 9, 0, 4, upper=np.nan)
+    x[0][np.tril(np.ones_like(x[0], bool), -1)] = 0.5
+    x[1][3, 1] = np.nan
+    x[1][7, 2:5] = np.nan
+    x[2] = np.where(np.tril(np.ones_like(x[2], bool), -1), np.float32(1.0), np.float32(7.0))
+    compare(g, x, [0.5, 0.0, 1.0, np.nextafter(np.float32(0.5), np.float32(0))], masks=True)
+
+
+def test_binary_patterns_closed_forms():
+    from tests.oracle_helpers import S_all, S_chen, S_liveness, S_zero
+    L = 16
+    g = G.training_chain(L)
+    pats = [S_zero(g.n), S_all(g.n), S_liveness(g), S_chen(L, [4, 8, 12])]
+    x = np.stack([from_binary(S) for S in pats])
+    res, _ = compare(g, x, [0.5])
+    n = g.n
+    assert list(res["cost"]) == [n * (n + 1) // 2, n, n, 46]
+    assert list(res["peak"]) == [L + 2, n, L + 2, 9]
+
+
+def test_index_base_and_total():
+    g = G.vgg16()
+    x = gen_sstar(g, "mix", 3, 0, 5)
+    compare(g, x, [0.5, 0.6], B.geometric_grid(g, 4), index_base=1000, total=5000)
+
+
+def test_empty_batch():
+    import torch
+    import paper_1910_02653_b200 as cm
+    g = G.path(8)
+    graph = cm.Graph.from_workload(g)
+    x = torch.zeros((0, 8, 8), device="cuda")
+    out = cm.round_and_evaluate(graph, x, torch.tensor([0.5], device="cuda"),
+                                torch.tensor([4], dtype=torch.int64, device="cuda"))
+    torch.cuda.synchronize()
+    assert out["peak"].numel() == 0 and int(out["best_key"][0]) == KEY_NONE
+
+
+def test_error_paths_on_device():
+    import torch
+    import paper_1910_02653_b200 as cm
+    g = G.path(8)
+    graph = cm.Graph.from_workload(g)
+    x = torch.zeros((2, 8, 8), device="cuda")
+    th = torch.tensor([0.5], device="cuda")
+    with pytest.raises(cm.CMError):
+        cm.round_and_evaluate(graph, x, th, ld=6)                   # ld < n
+    with pytest.raises(cm.CMError):
+        cm.round_and_evaluate(graph, x, th, ld=8, stride=60)        # stride < n*ld
+    with pytest.raises(cm.CMError):
+        cm.round_and_evaluate(graph, x, th, index_base=5, total_candidates=3)
+    big = G.path(64, cost=[1 << 40] * 64)
+    gb = cm.Graph.from_workload(big)
+    xb = torch.zeros((1, 64, 64), device="cuda")
+    with pytest.raises(cm.CMError):                                 # key cannot hold cost bound
+        cm.round_and_evaluate(gb, xb, th, total_candidates=1 << 20)
+
+
+def test_max_n():
+    """n = CM_NMAX = 1024 (32 words per row, 1024 threads)."""
+    g = G.random_dag(1024, 0.0015, 77)
+    x = gen_sstar(g, "g1", 3, 0, 2)
+    compare(g, x, [0.5], [B.p_live(g)])
+
+
+def test_device_generator_matches_host():
+    import torch
+    from workloads.device_gen import DeviceGenerator
+    for name, fam, layout in [("resnet50", "mix", "dense"), ("unet", "g1", "tri4"), ("vgg16", "g2", "dense")]:
+        g = G.NETWORKS[name]()
+        dg = DeviceGenerator(g, fam, 1234, layout=layout)
+        buf = torch.empty(dg.shape(6), dtype=torch.float32, device="cuda")
+        dg.fill(buf, s_begin=500, upper=0.0)
+        host = gen_sstar(g, fam, 1234, 500, 6, layout=layout)
+        assert np.array_equal(buf.cpu().numpy().view(np.uint32), host.view(np.uint32)), name
+
+
+def test_full_size_sampled():
+    """The bench launch configuration (ResNet-50, n=353, G1 LP-like S*, theta 0.5, 16 budgets,
+    device-generated batch) checked on sampled candidates against the oracle, plus the
+    per-budget keys against the GPU's own per-candidate outputs."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    g = G.resnet50()
+    N = 8192
+    dg = DeviceGenerator(g, "g1", 2024, layout="tri4")
+    buf = torch.empty(dg.shape(N), dtype=torch.float32, device="cuda")
+    dg.fill(buf, 0)
+    graph = cm.Graph.from_workload(g)
+    budgets = B.geometric_grid(g, 16)
+    bu = torch.tensor(budgets, device="cuda")
+    th = torch.tensor([0.5], device="cuda")
+    out = cm.round_and_evaluate(graph, buf, th, bu, layout="tri4")
+    torch.cuda.synchronize()
+    peak = out["peak"].cpu().numpy()
+    cost = out["cost"].cpu().numpy()
+    inst = Instance.from_graph(g)
+    rng = np.random.default_rng(0)
+    sample = sorted(set(rng.integers(0, N, 20).tolist()) | {0, N - 1})
+    for s in sample:
+        x = gen_sstar(g, "g1", 2024, s, 1)[0]
+        o = evaluate(inst, x, 0.5)
+        assert (peak[s], cost[s]) == (o["peak"], o["cost"]), s
+    bits = out["idx_bits"]
+    for b, key in enumerate(out["best_key"].cpu().numpy()):
+        feas = np.nonzero(peak <= budgets[b])[0]
+        if len(feas) == 0:
+            assert key == KEY_NONE
+            continue
+        c = cost[feas].min()
+        idx = feas[cost[feas] == c].min()
+        assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, idx)
+    # the winner of the loosest budget re-checked by the oracle
+    wi = int(out["best_key"][-1].item()) & ((1 << bits) - 1)
+    o = evaluate(inst, gen_sstar(g, "g1", 2024, wi, 1)[0], 0.5)
+    assert (o["peak"], o["cost"]) == (peak[wi], cost[wi])
