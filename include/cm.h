@@ -92,6 +92,9 @@ typedef struct {
                                (CM_KEY_NONE = nothing feasible yet) */
   uint64_t* r_mask;         /* device [n_cand][n][W], W = ceil(n/64), or NULL: R rows, bit i%64 of word i/64 */
   uint64_t* s_mask;         /* device [n_cand][n][W] or NULL: S rows */
+  void* workspace;          /* device scratch for the stage-sliced S columns, or NULL to use the
+                               graph's own (then calls sharing a graph must be stream-ordered) */
+  int64_t workspace_bytes;  /* size of `workspace`; >= cm_workspace_bytes(g, 1) */
 } cm_eval_args;
 
 /*
@@ -101,6 +104,10 @@ typedef struct {
  * cost bound no longer fits the key (cost_bound >= 2^(63 - idx_bits)).
  */
 cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* args, cm_stream stream);
+
+/* Bytes of workspace needed to process `chunk_candidates` candidates per internal chunk
+ * (the library splits a batch into chunks that fit the workspace it is given). */
+int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates);
 
 /* idx_bits used by the key packing: number of bits of (total_candidates - 1); 0 when total <= 1. */
 int32_t cm_key_idx_bits(int64_t total_candidates);

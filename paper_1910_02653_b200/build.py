@@ -1,6 +1,7 @@
 """In-tree build of the sm_100a shared libraries (nvcc; no JIT cache).
 
-    python -m paper_1910_02653_b200.build        # builds both libraries if stale
+    python paper_1910_02653_b200/build.py [--force]   # builds both libraries if stale
+    (run as a file: importing the package needs the library this produces)
 
 libcheckmate_b200.so   the product: C ABI of include/cm.h
 workloads/libcm_gen.so the device input generator (workloads/csrc/gen_sstar.cu)

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -11,6 +12,7 @@
 
 #include "cm.h"
 #include "cm_kernel.cuh"
+#include "cm_v2.cuh"
 
 namespace {
 
@@ -35,7 +37,176 @@ struct cm_graph {
   int32_t blob_bytes = 0;
   int32_t o_pred_ptr = 0, o_pred_idx = 0, o_later = 0, o_succ_ptr = 0, o_succ_idx = 0;
   void* d_blob = nullptr;
+  // v2 (stage-sliced) path
+  int32_t blob2_bytes = 0;            // M, C, pred_ptr, pred_idx only
+  void* d_blob2 = nullptr;
+  void* d_nib = nullptr;              // K1 nibble tables of M (checkpoint mass, Eq. 6)
+  int32_t nib_entries = 0;
+  void* d_ws = nullptr;               // default workspace: two chunk buffers of Sn columns
+  int64_t ws_bytes = 0;
+  // K1 (rounding) runs on its own stream so it streams chunk c+1 from HBM while K2 scans
+  // chunk c; events order the two buffers (ping-pong) against the caller's stream.
+  cudaStream_t st_round = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_round[2] = {nullptr, nullptr}, ev_scan[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  std::mutex mu;
 };
+
+namespace {
+int kernel_choice() {                 // CM_KERNEL=v1 selects the row-form kernel (A/B tests)
+  const char* e = std::getenv("CM_KERNEL");
+  return (e && std::strcmp(e, "v1") == 0) ? 1 : 2;
+}
+int cpw_override() {
+  const char* e = std::getenv("CM_CPW");
+  return e ? std::atoi(e) : 0;
+}
+constexpr int64_t kDefaultWsBytes = int64_t(96) << 20;   // two 48 MB chunks: L2-resident (126 MB L2)
+}  // namespace
+
+
+namespace {
+
+// Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
+int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
+size_t scan_warp_bytes(int n) { return (size_t)8 * 32 * 32 + (size_t)4 * 32 * ((n + 3) & ~3); }
+
+cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
+  const int n = g->n;
+  const int G = (n + 31) / 32;
+  const int cs = cm2::cand_words(n);
+  void* ws = a->workspace ? a->workspace : g->d_ws;
+  const int64_t ws_bytes = a->workspace ? a->workspace_bytes : g->ws_bytes;
+  if (a->workspace && (reinterpret_cast<uintptr_t>(a->workspace) & 15))
+    return fail(CM_EINVAL, "workspace not 16-byte aligned");
+  int64_t cap = ws_bytes / 2 / cand_bytes(n);                       // candidates per chunk buffer
+  cap &= ~int64_t(31);
+  if (cap < std::max<int64_t>(32, a->n_theta)) return fail(CM_EINVAL, "workspace too small");
+  const int64_t chunk_s = std::min<int64_t>(cap / a->n_theta, 1 << 20);   // S* per chunk
+
+  const size_t wb = scan_warp_bytes(n);
+  const size_t fixed = (size_t)g->blob2_bytes;
+  if (fixed + wb > (size_t)g->smem_optin) return fail(CM_ERANGE, "scan kernel: shared memory exceeded");
+  const int wpc = (int)std::min<size_t>(8, ((size_t)g->smem_optin - fixed) / wb);
+  const size_t smem2 = fixed + wb * wpc;
+
+  static std::mutex attr_mu;
+  static size_t set2 = 0;
+  cudaError_t e;
+  {
+    std::lock_guard<std::mutex> lock(attr_mu);
+    if (smem2 > set2) {
+      e = cudaFuncSetAttribute(cm2::scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(smem2, 48 * 1024));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(scan_kernel)");
+      set2 = smem2;
+    }
+  }
+  int occ1 = 0, occ2 = 0;
+  const size_t smem1 = 0;
+  {
+    // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~224 KB per SM).
+    static bool carve = false;
+    std::lock_guard<std::mutex> lock(attr_mu);
+    if (!carve) {
+      e = cudaFuncSetAttribute(cm2::scan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+      if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
+      carve = true;
+    }
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_pack_kernel, 256, smem1);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cm2::scan_kernel, 32 * wpc, smem2);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+  if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
+
+  cm2::RoundParams rp;
+  rp.sstar = a->sstar;
+  rp.layout = a->layout;
+  rp.ld = a->ld;
+  rp.stride = a->sstar_stride;
+  rp.n = n;
+  rp.G = G;
+  rp.n_theta = a->n_theta;
+  rp.theta = a->theta;
+  rp.bw = cm2::block_words(G);
+  rp.cs = cs;
+  rp.nib = reinterpret_cast<const int64_t*>(g->d_nib);
+  rp.nib_entries = g->nib_entries;
+  rp.brow = cm2::brow_off(n);
+
+  cm2::ScanParams sp;
+  sp.blob = reinterpret_cast<const uint4*>(g->d_blob2);
+  sp.blob_bytes = g->blob2_bytes;
+  sp.n = n;
+  sp.o_pred_ptr = 0;
+  sp.o_pred_idx = n + 1;
+  sp.cs = cs;
+  sp.G = G;
+  sp.brow = cm2::brow_off(n);
+  sp.r_mask32 = reinterpret_cast<uint32_t*>(a->r_mask);
+  sp.s_mask32 = reinterpret_cast<uint32_t*>(a->s_mask);
+  sp.warp_bytes = (int32_t)wb;
+
+  cm2::ReduceParams qp;
+  qp.G = G;
+  qp.index_base = a->index_base;
+  qp.ovh = g->ovh;
+  qp.idx_bits = idx_bits;
+  qp.n_budget = a->n_budget;
+  qp.budget = a->budget;
+  qp.peak = a->peak;
+  qp.cost = a->cost;
+  qp.best_key = a->best_key;
+
+  unsigned char* base = reinterpret_cast<unsigned char*>(ws);
+  const int64_t half = cap * cand_bytes(n);
+  std::lock_guard<std::mutex> lock(g->mu);
+  e = cudaEventRecord(g->ev_start, st);                       // inputs written on `st` before the call
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g->st_round, g->ev_start, 0);
+  int c = 0;
+  for (int64_t s0 = 0; s0 < a->n_sstar && e == cudaSuccess; s0 += chunk_s, ++c) {
+    const int b = c & 1;
+    const int sc = (int)std::min<int64_t>(chunk_s, a->n_sstar - s0);
+    const int64_t nc = (int64_t)sc * a->n_theta;
+    uint32_t* blk = reinterpret_cast<uint32_t*>(base + b * half);
+    int64_t* part = reinterpret_cast<int64_t*>(base + b * half + 4 * cap * (int64_t)cs);
+    if (g->used[b]) e = cudaStreamWaitEvent(g->st_round, g->ev_scan[b], 0);   // buffer b drained
+    if (e != cudaSuccess) break;
+    rp.s_begin = s0;
+    rp.s_count = sc;
+    rp.sn = blk;
+    const int64_t warps1 = (int64_t)sc * G;
+    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + 7) / 8, (int64_t)occ1 * g->sm_count));
+    for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
+      rp.th0 = th0;
+      rp.nt = std::min(4, a->n_theta - th0);
+      cm2::round_pack_kernel<<<grid1, 256, smem1, g->st_round>>>(rp);
+    }
+    e = cudaEventRecord(g->ev_round[b], g->st_round);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_round[b], 0);
+    if (e != cudaSuccess) break;
+    sp.ws = blk;
+    sp.n_cand = nc;
+    sp.n_batch = (int)((nc + 31) / 32);
+    sp.part = part;
+    sp.out_base = s0 * a->n_theta;
+    const int64_t tasks = (int64_t)G * sp.n_batch;
+    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + wpc - 1) / wpc, (int64_t)occ2 * g->sm_count));
+    cm2::scan_kernel<<<grid2, 32 * wpc, smem2, st>>>(sp);
+    qp.part = part;
+    qp.n_cand = nc;
+    qp.out_base = sp.out_base;
+    cm2::reduce_kernel<<<(int)((nc + 255) / 256), 256, 0, st>>>(qp);
+    e = cudaEventRecord(g->ev_scan[b], st);
+    g->used[b] = true;
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "launch v2 kernels");
+  return CM_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -180,14 +351,67 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     delete g;
     return cuda_fail(e, "cm_graph_create: cudaMemcpy");
   }
+  // v2 blob: M[n], C[n] int64, pred_ptr[n+1], pred_idx[E]
+  size_t bytes2 = 16 * (size_t)n + 4 * (size_t)(n + 1 + E);
+  bytes2 = (bytes2 + 15) & ~size_t(15);
+  g->blob2_bytes = (int32_t)bytes2;
+  std::vector<unsigned char> blob2(bytes2, 0);
+  std::memcpy(blob2.data(), blob.data(), 16 * (size_t)n + 4 * (size_t)(n + 1 + E));
+  e = cudaMalloc(&g->d_blob2, bytes2);
+  if (e == cudaSuccess) e = cudaMemcpy(g->d_blob2, blob2.data(), bytes2, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    g->nib_entries = 128 * ((n + 31) / 32);            // 8 nibbles per 32-node block, every block
+    std::vector<int64_t> nib(g->nib_entries, 0);
+    for (int q = 0; q < g->nib_entries / 16; ++q)
+      for (int v = 0; v < 16; ++v)
+        for (int j = 0; j < 4; ++j)
+          if ((v >> j) & 1 && 4 * q + j < n) nib[16 * q + v] += mem[4 * q + j];
+    e = cudaMalloc(&g->d_nib, 8 * (size_t)g->nib_entries);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_nib, nib.data(), 8 * (size_t)g->nib_entries, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) {
+    const int64_t per = cand_bytes(n);
+    g->ws_bytes = std::max<int64_t>(per * 1024, (kDefaultWsBytes / (64 * per)) * 64 * per);
+    e = cudaMalloc(&g->d_ws, g->ws_bytes);
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->st_round, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaEventCreateWithFlags(&g->ev_round[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_scan[b], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (g->d_blob2) cudaFree(g->d_blob2);
+    if (g->d_ws) cudaFree(g->d_ws);
+    if (g->d_nib) cudaFree(g->d_nib);
+    cudaFree(g->d_blob);
+    delete g;
+    return fail(CM_ENOMEM, std::string("cm_graph_create: ") + cudaGetErrorString(e));
+  }
   *out = g;
   return CM_OK;
 }
 
 void cm_graph_destroy(cm_graph* g) {
   if (!g) return;
+  if (g->st_round) cudaStreamSynchronize(g->st_round);
+  for (int b = 0; b < 2; ++b) {
+    if (g->ev_round[b]) cudaEventDestroy(g->ev_round[b]);
+    if (g->ev_scan[b]) cudaEventDestroy(g->ev_scan[b]);
+  }
+  if (g->ev_start) cudaEventDestroy(g->ev_start);
+  if (g->st_round) cudaStreamDestroy(g->st_round);
   if (g->d_blob) cudaFree(g->d_blob);
+  if (g->d_blob2) cudaFree(g->d_blob2);
+  if (g->d_ws) cudaFree(g->d_ws);
+  if (g->d_nib) cudaFree(g->d_nib);
   delete g;
+}
+
+int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {
+  if (!g || chunk_candidates < 1) return -1;
+  return 2 * cand_bytes(g->n) * ((chunk_candidates + 31) & ~int64_t(31));   // two buffers
 }
 
 int32_t cm_graph_n(const cm_graph* g) { return g ? g->n : -1; }
@@ -222,6 +446,11 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
   if (n_cand == 0) return CM_OK;
+  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n) <= (size_t)g->smem_optin) {
+    cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
+    if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
+    return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);
+  }
 
   const int G = (n + 31) / 32;
   const int tri_words = 16 * G * (G + 1);

@@ -1,0 +1,382 @@
+// cm_v2.cuh -- stage-sliced sm_100a kernels for Checkmate two-phase rounding (Alg. 2,
+// PAPER.md:389-415) and the Eq. 6-9 memory accounting.
+//
+// "Stage-sliced": a 32-bit word holds one node's bit for 32 consecutive stages.  A lane
+// owns a group g of 32 stages (rows 32g..32g+31, 0-based row r = stage t-1) of one
+// candidate, so every bitwise step of the method runs for 32 stages at once and the control
+// flow (a walk over the graph) is identical in all lanes: no per-stage divergence, however
+// recomputation is distributed over the stages.
+//
+// K1 round_pack_kernel (HBM-bound).  Task = (S*, row group g).  For each 32x32 block
+//   (w = 0..g) lane l loads row r = 32g+l+1 with 16-byte streaming loads, compares > theta
+//   (a1: strict, fp32, NaN -> 0) into a row word, and a 5-step shuffle
+//   transpose turns the 32 row words into column words
+//       Sn_g[i]  bit b = S_{row 32g+b+1, node i} = S_{t+1}   for stage t = 32g+b+1,
+//   i.e. the NEXT stage's checkpoint bits (S_{n+1} = 0).  The current stage's
+//   bits follow from them: Sw_g = (Sn_g << 1) | (Sn_{g-1} >> 31).  One S* read serves every
+//   threshold.
+//
+// K2 scan_kernel (ALU / latency-bound).  One warp evaluates cpw candidates, lanes =
+//   (candidate, group).  A single pass over nodes k = n-1 .. 0 (reverse topological order,
+//   the paper's right-to-left repair scan), push form:
+//     R_k   = ((Sn_k | Acc_k) & ~Sw_k) | diag_k      a2 seed S_{t+1} & ~S_t, e_t; a3 closure
+//             Acc_k = OR of R_j over the users j > k (all visited before k)
+//     FREE  i in DEPS(k): R_k & ~Sn_i & ~Acc_i       Eq. 9: k computed, i not kept, no later user
+//           i = k:        R_k & ~Sn_k & ~Acc_k       the i = k term of Eq. 8
+//     Acc_i |= R_k
+//   Memory: with D = U_{t,k} - U_{t,end} run backwards and MX = max over computes of D,
+//   only E = MX - D matters:  frees:  E -= M_i ;  compute of k:  E = max(E, 0) + M_k.
+//   Then peak_t = U_{t,0} + E_t (the max over k is reached at a compute,
+//   DESIGN.md Q9), with U_{t,0} = ovh + mass_t (Eq. 6) from K1.  The per-stage int64 E sits
+//   in shared memory and is touched only at set bits (events).
+//
+// Layout of one candidate's column array in the workspace: group g holds nodes 0..32g+31 at
+// word offset grp_off(g) = 16 g (g+1) (16-byte aligned).
+#pragma once
+#include <stdint.h>
+
+namespace cm2 {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ __forceinline__ int grp_off(int g) { return 16 * g * (g + 1); }
+__host__ __device__ __forceinline__ int block_words(int G) { return 16 * G * (G + 1); }
+// workspace words per candidate: [Sn columns: block_words][mass: n int64][brow: G x G u32]
+// brow row g = the row-form words of S row 32g (bits over nodes), the bit S_t for t = 32g+1
+// that a group-g pass cannot derive from its own Sn columns.
+__host__ __device__ __forceinline__ int cand_words(int n) {
+  const int G = (n + 31) / 32;
+  return (block_words(G) + 2 * n + G * G + 3) & ~3;
+}
+__host__ __device__ __forceinline__ int brow_off(int n) { return block_words((n + 31) / 32) + 2 * n; }
+
+__device__ __forceinline__ int64_t row_offset(int layout, int64_t ld, int r) {
+  if (layout == 0) return (int64_t)r * ld;
+  const int64_t q = r >> 2, m = r & 3;                     // sum_{r'<r} roundup4(r')
+  return 8 * q * (q - 1) + 12 * q + (m > 0 ? 4 * q : 0) + (m > 1 ? (m - 1) * (4 * q + 4) : 0);
+}
+
+// 32x32 bit transpose across a warp: in, lane l holds row word l (bit c = A[l][c]);
+// out, lane l holds column word l (bit r = A[r][l]).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+    const uint32_t M = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                     : j == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(FULL, x, j);
+    const bool hi = (lane & j) != 0;
+    const uint32_t t = hi ? (y >> j) : (y << j);
+    const uint32_t K = hi ? ~M : M;
+    x = (x & K) | (t & ~K);
+  }
+  return x;
+}
+
+// ------------------------------------------------------------------------------------ K1
+struct RoundParams {
+  const float* sstar;
+  int32_t layout;
+  int64_t ld, stride;
+  int32_t n, G;
+  int64_t s_begin;            // first S* of this chunk (batch-relative)
+  int32_t s_count;
+  int32_t n_theta;            // all thresholds (block index stride)
+  int32_t th0, nt;            // this launch handles thresholds th0 .. th0+nt-1, nt <= 4
+  const float* theta;
+  uint32_t* sn;               // out: candidate block (s - s_begin) * n_theta + j, cs words each:
+  int32_t cs;                 //   [Sn columns: bw words][mass: n int64]
+  int32_t bw;
+  const int64_t* nib;         // nibble tables: nib[p*16 + v] = sum_{j<4, bit j of v} M[4p + j]
+  int32_t nib_entries;        // 128 * G
+  int32_t brow;               // word offset of brow in a candidate block
+};
+
+// Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31 (the S_{t+1} rows of the
+// group's stages), 32 nodes (block w) at a time.  Lane = node: row q of the block is one
+// coalesced 128-byte load, one compare (a1, strict fp32 '>', NaN -> 0) and one ballot, which
+// is already the packed row word.  The 32 row words go through a 32-word shared slot to
+// lane q, which transposes them into column words and adds the checkpoint mass of its
+// row, mass_r = sum_{i in S_r} M_i (the Eq. 6 sum), from 4-bit tables.
+// Out-of-triangle elements are replaced by NaN, which compares false for every theta.
+__global__ void __launch_bounds__(256) round_pack_kernel(const RoundParams p) {
+  __shared__ uint32_t rows_w[8][32];                              // per-warp ballot slot
+  __shared__ int64_t rows_off[8][32];                             // per-warp row offsets
+  const int64_t* nib = p.nib;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const int tasks = p.s_count * p.G;
+  const float qnan = __int_as_float(0x7fffffff);
+  for (int task = wid; task < tasks; task += nw) {
+    const int s = task / p.G;
+    const int g = task - s * p.G;
+    const float* S0 = p.sstar + (p.s_begin + s) * p.stride;
+    uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
+    const int rq = 32 * g + lane + 1;                               // row owned by this lane
+    rows_off[wl][lane] = row_offset(p.layout, p.ld, rq);
+    __syncwarp();
+    const bool full_rows = (32 * g + 32) < p.n;                     // every r_q exists
+    int64_t mass[4] = {0, 0, 0, 0};
+    for (int w = 0; w <= g; ++w) {
+      const int node = 32 * w + lane;
+      float x[32];
+      if (w < g && full_rows) {                                     // interior block: no masking
+#pragma unroll
+        for (int q = 0; q < 32; ++q) x[q] = __ldcs(S0 + rows_off[wl][q] + node);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int r = 32 * g + 1 + q;
+          x[q] = (r < p.n && node < r) ? __ldcs(S0 + rows_off[wl][q] + node) : qnan;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= p.nt) break;
+        const float th = __ldg(p.theta + p.th0 + j);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const uint32_t b = __ballot_sync(FULL, x[q] > th);
+          rows_w[wl][q] = b;                                        // uniform value: one store
+        }
+        __syncwarp();
+        const uint32_t word = rows_w[wl][lane];                     // row r_q's word, block w
+        __syncwarp();
+        int64_t ms = 0;
+        if (word) {
+          const int64_t* tw = nib + 128 * w;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+        }
+        uint32_t* oj = out + (int64_t)j * p.cs;
+        if (lane == 31 && g + 1 < p.G) oj[p.brow + (g + 1) * p.G + w] = word;   // row 32(g+1)
+        oj[grp_off(g) + node] = transpose32(word, lane);
+        mass[j] += ms;
+      }
+    }
+    if (rq < p.n) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------ K2
+// Group-major scan: a task is (stage group g, 32 candidates); lane l works on candidate
+// c0 + l.  The stages of different groups never interact (stage t needs only S_t, S_{t+1}
+// and the graph), so a group pass is a complete, independent evaluation of its 32 stages;
+// all lanes walk the same node range k = min(n,32g+32)-1 .. 0 in lockstep.
+// Shared memory per warp: Sn[node][lane], Acc[node][lane] (u32) and E[stage][lane] (int64),
+// every access lane-contiguous (bank-conflict free).
+struct ScanParams {
+  const uint4* blob;          // M[n] int64, C[n] int64, pred_ptr[n+1], pred_idx[E] (int32)
+  int32_t blob_bytes;
+  int32_t n, o_pred_ptr, o_pred_idx;
+  const uint32_t* ws;         // chunk workspace from K1 (cs words per candidate)
+  int32_t cs, G, brow;
+  int64_t n_cand;             // candidates in this chunk
+  int32_t n_batch;            // ceil(n_cand / 32)
+  int64_t* part;              // out: [n_cand][G] x {peak_g - ovh, cost_g}
+  uint32_t* r_mask32;         // optional masks (u64 words seen as pairs of u32)
+  uint32_t* s_mask32;
+  int64_t out_base;           // local index of the chunk's first candidate
+  int32_t warp_bytes;         // shared bytes per warp region
+};
+
+// One node k of the group-g pass for dependency count ND (0..4; ND = 4 also walks any
+// further dependencies).  Specialised so the event loop carries exactly ND free masks.
+template <int ND>
+__device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, int64_t Mk, int e0, int nd,
+                                          const int32_t* __restrict__ pred_idx,
+                                          const int64_t* __restrict__ M, uint32_t* A, int64_t* E,
+                                          int lane, uint32_t& a_next) {
+  uint32_t f[ND > 0 ? ND : 1];
+  int64_t mi[ND > 0 ? ND : 1];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) {                                   // FREE_{t,i,k} = R_k & ~A'_i
+    const int i = pred_idx[e0 + j];
+    const bool nb = (i == k - 1);
+    const uint32_t ai = nb ? a_next : A[32 * i + lane];
+    f[j] = Rk & ~ai;
+    A[32 * i + lane] = ai | Rk;                                     // A'_i |= R_k
+    if (nb) a_next = ai | Rk;
+    mi[j] = M[i];
+  }
+  if (ND == 4) {
+    for (int e = e0 + 4; e < e0 + nd; ++e) {                       // in-degree > 4 (rare)
+      const int i = pred_idx[e];
+      const bool nb = (i == k - 1);
+      const uint32_t ai = nb ? a_next : A[32 * i + lane];
+      uint32_t fx = Rk & ~ai;
+      A[32 * i + lane] = ai | Rk;
+      if (nb) a_next = ai | Rk;
+      const int64_t Mi = M[i];
+      for (; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
+    }
+  }
+  const uint32_t selff = Rk & ~a;                                   // FREE_{t,k,k}
+  // every free at k lies in a stage that computes k: E = max(E - GC(k), 0) + M_k
+  for (uint32_t x = Rk; x; x &= x - 1) {
+    const int b = __ffs(x) - 1;
+    int64_t ev = E[32 * b + lane];
+    if ((selff >> b) & 1u) ev -= Mk;
+#pragma unroll
+    for (int j = 0; j < ND; ++j)
+      if ((f[j] >> b) & 1u) ev -= mi[j];
+    E[32 * b + lane] = (ev > 0 ? ev : 0) + Mk;
+  }
+}
+
+__global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = p.n, G = p.G;
+  const int64_t* M = reinterpret_cast<const int64_t*>(smem);
+  const int64_t* C = M + n;
+  const int32_t* gi = reinterpret_cast<const int32_t*>(smem + 16 * n);
+  const int32_t* pred_ptr = gi + p.o_pred_ptr;
+  const int32_t* pred_idx = gi + p.o_pred_idx;
+  unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
+  int64_t* E = reinterpret_cast<int64_t*>(wr);                     // [32 stages][32 lanes]
+  uint32_t* A = reinterpret_cast<uint32_t*>(E + 32 * 32);           // [node][lane]: Sn | Acc, then R
+  for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
+  __syncthreads();
+
+  const int tasks = G * p.n_batch;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int task = gw; task < tasks; task += nwarps) {
+    const int g = G - 1 - task / p.n_batch;                         // big groups first
+    const int64_t c = (int64_t)(task % p.n_batch) * 32 + lane;
+    const bool live = c < p.n_cand;
+    const int nk = min(n, 32 * (g + 1));                            // nodes 0..nk-1
+    const int nq = (nk + 3) >> 2;                                   // uint4 blocks of Sn
+    const uint32_t* cw = p.ws + (live ? c : 0) * p.cs;
+    const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
+    // A'_i = Sn_i | Acc_i (Acc = OR of R over visited users): the closure reads Sn_k | Acc_k and
+    // every FREE test reads Sn_i | Acc_i, so one array serves both.  Start: A' = Sn.
+    for (int q = 0; q < nq; ++q) {
+      const uint4 v = live ? __ldcg(sn4 + q) : make_uint4(0u, 0u, 0u, 0u);
+      const int i0 = 4 * q;
+      A[32 * i0 + lane] = v.x;
+      if (i0 + 1 < nk) A[32 * (i0 + 1) + lane] = v.y;
+      if (i0 + 2 < nk) A[32 * (i0 + 2) + lane] = v.z;
+      if (i0 + 3 < nk) A[32 * (i0 + 3) + lane] = v.w;
+    }
+    for (int b = 0; b < 32; ++b) E[32 * b + lane] = 0;
+    __syncwarp();
+    const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
+    int64_t costL = 0;
+    uint4 cur = live ? __ldcg(sn4 + nq - 1) : make_uint4(0u, 0u, 0u, 0u);
+    uint32_t a_next = A[32 * (nk - 1) + lane];
+    for (int q = nq - 1; q >= 0; --q) {
+      const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t bword = (g > 0 && (q >> 3) < g && live) ? brow[q >> 3] : 0u;
+#pragma unroll
+      for (int u = 3; u >= 0; --u) {
+        const int k = 4 * q + u;
+        if (k >= nk) continue;                                      // warp-uniform
+        const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
+        const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);  // S_t from S_{t+1} and row 32g
+        const uint32_t a = a_next;                                  // A'_k = Sn_k | Acc_k (complete)
+        a_next = k > 0 ? A[32 * (k - 1) + lane] : 0u;               // prefetch; fixed up on a push
+        const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
+        const uint32_t Rk = (a & ~sw) | diag;                       // a2 seed + a3 closure
+        A[32 * k + lane] = Rk;                                      // slot now holds R column
+        const int64_t Mk = M[k];
+        costL += (int64_t)__popc(Rk) * C[k];
+        const int e0 = pred_ptr[k], nd = pred_ptr[k + 1] - e0;
+        switch (nd) {                                               // warp-uniform
+          case 0: node_step<0>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 1: node_step<1>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 2: node_step<2>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 3: node_step<3>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          default: node_step<4>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+        }
+      }
+      cur = nxt;
+    }
+    // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
+    const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
+    int64_t pk = INT64_MIN;
+    for (int b = 0; b < 32 && 32 * g + b < n; ++b) {
+      const int r = 32 * g + b;
+      const int64_t m = (r && live) ? __ldcg(mass + r) : 0;
+      pk = max(pk, m + E[32 * b + lane]);
+    }
+    if (live) {
+      int64_t* pp = p.part + 2 * (c * G + g);
+      pp[0] = pk;
+      pp[1] = costL;
+    }
+    if (p.r_mask32 || p.s_mask32) {                                 // verification output
+      __syncwarp();
+      const int W32 = 2 * ((n + 63) >> 6);
+      for (int cl = 0; cl < 32; ++cl) {
+        const int64_t cc = (int64_t)(task % p.n_batch) * 32 + cl;
+        if (cc >= p.n_cand) break;                                  // warp-uniform
+        const uint32_t* ccw = p.ws + cc * p.cs;
+        const int row = 32 * g + lane;
+        for (int w = 0; w < W32; ++w) {
+          uint32_t xr = 0, xs = 0;
+          if (w <= g) {
+            const int node = 32 * w + lane;
+            const uint32_t rc = node < nk ? A[32 * node + cl] : 0u;
+            uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
+            const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
+            sc = (sc << 1) | ((bb >> lane) & 1u);
+            xr = transpose32(rc, lane);
+            xs = transpose32(sc, lane);
+          }
+          if (row < n) {
+            const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32 + w;
+            if (p.r_mask32) p.r_mask32[o] = xr;
+            if (p.s_mask32) p.s_mask32[o] = xs;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------ K3
+// Per candidate: peak = ovh + max_g part_peak, cost = sum_g part_cost; then the a7 keys.
+struct ReduceParams {
+  const int64_t* part;
+  int32_t G;
+  int64_t n_cand, out_base, index_base;
+  int64_t ovh;
+  int32_t idx_bits, n_budget;
+  const int64_t* budget;
+  int64_t* peak;
+  int64_t* cost;
+  int64_t* best_key;
+};
+
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= p.n_cand) return;
+  const int64_t* pp = p.part + 2 * c * p.G;
+  int64_t pk = INT64_MIN, cs = 0;
+  for (int g = 0; g < p.G; ++g) {
+    pk = max(pk, __ldcg(pp + 2 * g));
+    cs += __ldcg(pp + 2 * g + 1);
+  }
+  pk += p.ovh;
+  const int64_t local = p.out_base + c;
+  p.peak[local] = pk;
+  p.cost[local] = cs;
+  const int64_t key = (cs << p.idx_bits) | (p.index_base + local);
+  for (int b = 0; b < p.n_budget; ++b) {
+    if (pk <= __ldg(p.budget + b)) {
+      const int64_t cur = *reinterpret_cast<volatile const int64_t*>(p.best_key + b);
+      if (key < cur) atomicMin(reinterpret_cast<long long*>(p.best_key + b), (long long)key);
+    }
+  }
+}
+
+}  // namespace cm2

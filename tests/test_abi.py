@@ -13,8 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_1910_02653_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__.build()
     from paper_1910_02653_b200 import _abi
     return _abi.load()
 
