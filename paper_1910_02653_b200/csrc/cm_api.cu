@@ -38,7 +38,9 @@ struct cm_graph {
   int32_t o_pred_ptr = 0, o_pred_idx = 0, o_later = 0, o_succ_ptr = 0, o_succ_idx = 0;
   void* d_blob = nullptr;
   // v2 (stage-sliced) path
-  int32_t blob2_bytes = 0;            // M, C, pred_ptr, pred_idx only
+  int32_t blob2_bytes = 0;            // M/mscale, C, pred_ptr, pred_idx only
+  int64_t mscale = 1;                 // gcd of all M (>= 1); the scan works in units of it
+  bool scan32 = false;                // sum M / mscale < 2^30: int32 per-stage state
   void* d_blob2 = nullptr;
   void* d_nib = nullptr;              // K1 nibble tables of M (checkpoint mass, Eq. 6)
   int32_t nib_entries = 0;
@@ -69,7 +71,7 @@ namespace {
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
-size_t scan_warp_bytes(int n) { return (size_t)8 * 32 * 32 + (size_t)4 * 32 * ((n + 3) & ~3); }
+size_t scan_warp_bytes(int n, bool s32) { return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * ((n + 3) & ~3); }
 
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
@@ -84,7 +86,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   if (cap < std::max<int64_t>(32, a->n_theta)) return fail(CM_EINVAL, "workspace too small");
   const int64_t chunk_s = std::min<int64_t>(cap / a->n_theta, 1 << 20);   // S* per chunk
 
-  const size_t wb = scan_warp_bytes(n);
+  const size_t wb = scan_warp_bytes(n, g->scan32);
+  const void* scan_fn = g->scan32 ? reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>)
+                                  : reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>);
   const size_t fixed = (size_t)g->blob2_bytes;
   if (fixed + wb > (size_t)g->smem_optin) return fail(CM_ERANGE, "scan kernel: shared memory exceeded");
   const int wpc = (int)std::min<size_t>(8, ((size_t)g->smem_optin - fixed) / wb);
@@ -96,9 +100,12 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   {
     std::lock_guard<std::mutex> lock(attr_mu);
     if (smem2 > set2) {
-      e = cudaFuncSetAttribute(cm2::scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)std::max<size_t>(smem2, 48 * 1024));
-      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(scan_kernel)");
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>)}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(smem2, 48 * 1024));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(scan_kernel)");
+      }
       set2 = smem2;
     }
   }
@@ -109,14 +116,17 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
-      e = cudaFuncSetAttribute(cm2::scan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-      if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>)}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
+      }
       carve = true;
     }
   }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_pack_kernel, 256, smem1);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cm2::scan_kernel, 32 * wpc, smem2);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
 
@@ -152,6 +162,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   qp.G = G;
   qp.index_base = a->index_base;
   qp.ovh = g->ovh;
+  qp.mscale = g->mscale;
   qp.idx_bits = idx_bits;
   qp.n_budget = a->n_budget;
   qp.budget = a->budget;
@@ -193,7 +204,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     sp.out_base = s0 * a->n_theta;
     const int64_t tasks = (int64_t)G * sp.n_batch;
     const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + wpc - 1) / wpc, (int64_t)occ2 * g->sm_count));
-    cm2::scan_kernel<<<grid2, 32 * wpc, smem2, st>>>(sp);
+    if (g->scan32) cm2::scan_kernel<int32_t><<<grid2, 32 * wpc, smem2, st>>>(sp);
+    else cm2::scan_kernel<int64_t><<<grid2, 32 * wpc, smem2, st>>>(sp);
     qp.part = part;
     qp.n_cand = nc;
     qp.out_base = sp.out_base;
@@ -351,12 +363,26 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     delete g;
     return cuda_fail(e, "cm_graph_create: cudaMemcpy");
   }
-  // v2 blob: M[n], C[n] int64, pred_ptr[n+1], pred_idx[E]
+  // v2 blob: M[n]/mscale, C[n] int64, pred_ptr[n+1], pred_idx[E]
+  {
+    int64_t gd = 0;
+    for (int i = 0; i < n; ++i) {
+      int64_t a = mem[i], b = gd;
+      while (b) { const int64_t t = a % b; a = b; b = t; }
+      gd = a;
+    }
+    g->mscale = gd > 0 ? gd : 1;
+    int64_t tot = 0;
+    for (int i = 0; i < n; ++i) tot += mem[i] / g->mscale;
+    g->scan32 = tot < (int64_t(1) << 30);
+    if (!g->scan32) g->mscale = 1;
+  }
   size_t bytes2 = 16 * (size_t)n + 4 * (size_t)(n + 1 + E);
   bytes2 = (bytes2 + 15) & ~size_t(15);
   g->blob2_bytes = (int32_t)bytes2;
   std::vector<unsigned char> blob2(bytes2, 0);
   std::memcpy(blob2.data(), blob.data(), 16 * (size_t)n + 4 * (size_t)(n + 1 + E));
+  for (int i = 0; i < n; ++i) reinterpret_cast<int64_t*>(blob2.data())[i] = mem[i] / g->mscale;
   e = cudaMalloc(&g->d_blob2, bytes2);
   if (e == cudaSuccess) e = cudaMemcpy(g->d_blob2, blob2.data(), bytes2, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
@@ -365,7 +391,7 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     for (int q = 0; q < g->nib_entries / 16; ++q)
       for (int v = 0; v < 16; ++v)
         for (int j = 0; j < 4; ++j)
-          if ((v >> j) & 1 && 4 * q + j < n) nib[16 * q + v] += mem[4 * q + j];
+          if ((v >> j) & 1 && 4 * q + j < n) nib[16 * q + v] += mem[4 * q + j] / g->mscale;
     e = cudaMalloc(&g->d_nib, 8 * (size_t)g->nib_entries);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_nib, nib.data(), 8 * (size_t)g->nib_entries, cudaMemcpyHostToDevice);
   }
@@ -446,7 +472,7 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
   if (n_cand == 0) return CM_OK;
-  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n) <= (size_t)g->smem_optin) {
+  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n, g->scan32) <= (size_t)g->smem_optin) {
     cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);

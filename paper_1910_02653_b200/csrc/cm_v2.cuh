@@ -187,13 +187,13 @@ struct ScanParams {
 
 // One node k of the group-g pass for dependency count ND (0..4; ND = 4 also walks any
 // further dependencies).  Specialised so the event loop carries exactly ND free masks.
-template <int ND>
-__device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, int64_t Mk, int e0, int nd,
+template <int ND, typename ET>
+__device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk, int e0, int nd,
                                           const int32_t* __restrict__ pred_idx,
-                                          const int64_t* __restrict__ M, uint32_t* A, int64_t* E,
+                                          const int64_t* __restrict__ M, uint32_t* A, ET* E,
                                           int lane, uint32_t& a_next) {
   uint32_t f[ND > 0 ? ND : 1];
-  int64_t mi[ND > 0 ? ND : 1];
+  ET mi[ND > 0 ? ND : 1];
 #pragma unroll
   for (int j = 0; j < ND; ++j) {                                   // FREE_{t,i,k} = R_k & ~A'_i
     const int i = pred_idx[e0 + j];
@@ -202,7 +202,7 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, int64_
     f[j] = Rk & ~ai;
     A[32 * i + lane] = ai | Rk;                                     // A'_i |= R_k
     if (nb) a_next = ai | Rk;
-    mi[j] = M[i];
+    mi[j] = (ET)M[i];
   }
   if (ND == 4) {
     for (int e = e0 + 4; e < e0 + nd; ++e) {                       // in-degree > 4 (rare)
@@ -212,7 +212,7 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, int64_
       uint32_t fx = Rk & ~ai;
       A[32 * i + lane] = ai | Rk;
       if (nb) a_next = ai | Rk;
-      const int64_t Mi = M[i];
+      const ET Mi = (ET)M[i];
       for (; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
     }
   }
@@ -220,15 +220,18 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, int64_
   // every free at k lies in a stage that computes k: E = max(E - GC(k), 0) + M_k
   for (uint32_t x = Rk; x; x &= x - 1) {
     const int b = __ffs(x) - 1;
-    int64_t ev = E[32 * b + lane];
+    ET ev = E[32 * b + lane];
     if ((selff >> b) & 1u) ev -= Mk;
 #pragma unroll
     for (int j = 0; j < ND; ++j)
       if ((f[j] >> b) & 1u) ev -= mi[j];
-    E[32 * b + lane] = (ev > 0 ? ev : 0) + Mk;
+    E[32 * b + lane] = (ev > 0 ? ev : (ET)0) + Mk;
   }
 }
 
+// ET = int32_t when every M is a multiple of a scale s with sum M/s < 2^30 (the host checks;
+// exact), else int64_t.  M in the blob, the masses and the results are in units of s.
+template <typename ET>
 __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
   const int32_t* pred_ptr = gi + p.o_pred_ptr;
   const int32_t* pred_idx = gi + p.o_pred_idx;
   unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
-  int64_t* E = reinterpret_cast<int64_t*>(wr);                     // [32 stages][32 lanes]
+  ET* E = reinterpret_cast<ET*>(wr);                               // [32 stages][32 lanes]
   uint32_t* A = reinterpret_cast<uint32_t*>(E + 32 * 32);           // [node][lane]: Sn | Acc, then R
   for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
       if (i0 + 2 < nk) A[32 * (i0 + 2) + lane] = v.z;
       if (i0 + 3 < nk) A[32 * (i0 + 3) + lane] = v.w;
     }
-    for (int b = 0; b < 32; ++b) E[32 * b + lane] = 0;
+    for (int b = 0; b < 32; ++b) E[32 * b + lane] = (ET)0;
     __syncwarp();
     const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
     int64_t costL = 0;
@@ -286,15 +289,15 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
         const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
         const uint32_t Rk = (a & ~sw) | diag;                       // a2 seed + a3 closure
         A[32 * k + lane] = Rk;                                      // slot now holds R column
-        const int64_t Mk = M[k];
+        const ET Mk = (ET)M[k];
         costL += (int64_t)__popc(Rk) * C[k];
         const int e0 = pred_ptr[k], nd = pred_ptr[k + 1] - e0;
         switch (nd) {                                               // warp-uniform
-          case 0: node_step<0>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 1: node_step<1>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 2: node_step<2>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 3: node_step<3>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          default: node_step<4>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 0: node_step<0, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 1: node_step<1, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 2: node_step<2, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 3: node_step<3, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          default: node_step<4, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
         }
       }
       cur = nxt;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     for (int b = 0; b < 32 && 32 * g + b < n; ++b) {
       const int r = 32 * g + b;
       const int64_t m = (r && live) ? __ldcg(mass + r) : 0;
-      pk = max(pk, m + E[32 * b + lane]);
+      pk = max(pk, m + (int64_t)E[32 * b + lane]);
     }
     if (live) {
       int64_t* pp = p.part + 2 * (c * G + g);
@@ -349,7 +352,7 @@ struct ReduceParams {
   const int64_t* part;
   int32_t G;
   int64_t n_cand, out_base, index_base;
-  int64_t ovh;
+  int64_t ovh, mscale;        // peak = ovh + mscale * max_g part
   int32_t idx_bits, n_budget;
   const int64_t* budget;
   int64_t* peak;
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
     pk = max(pk, __ldcg(pp + 2 * g));
     cs += __ldcg(pp + 2 * g + 1);
   }
-  pk += p.ovh;
+  pk = p.ovh + p.mscale * pk;
   const int64_t local = p.out_base + c;
   p.peak[local] = pk;
   p.cost[local] = cs;

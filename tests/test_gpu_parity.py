@@ -236,3 +236,20 @@ def test_full_size_sampled():
     wi = int(out["best_key"][-1].item()) & ((1 << bits) - 1)
     o = evaluate(inst, gen_sstar(g, "g1", 2024, wi, 1)[0], 0.5)
     assert (o["peak"], o["cost"]) == (peak[wi], cost[wi])
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_int64_state_path(seed):
+    """M values too large for the int32 scan state (sum M / gcd >= 2^30): int64 kernels."""
+    g = G.random_training(20, 0.1, seed)
+    g.mem = g.mem * (1 << 35) + np.arange(g.n, dtype=np.int64) * 7 + 3    # gcd 1, huge sums
+    x = gen_sstar(g, "mix", 4, 0, 6)
+    compare(g, x, [0.5, 0.7], [B.p_floor(g), B.p_live(g)], masks=True)
+
+
+def test_scaled_int32_path():
+    """All M share a large common factor: the scan runs in units of gcd(M) exactly."""
+    g = G.resnet50()
+    g.mem = g.mem * 1000                                   # sum M >> 2^31, sum M / gcd small
+    x = gen_sstar(g, "g1", 8, 0, 3)
+    compare(g, x, [0.5], B.geometric_grid(g, 8))
