@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
     ap.add_argument("--family", default=None)
     ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
-    ap.add_argument("--layout", default="tri4", choices=["tri4", "dense"])
+    ap.add_argument("--layout", default="dense", choices=["tri4", "dense"])
     ap.add_argument("--e2e-batch", type=int, default=16384)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

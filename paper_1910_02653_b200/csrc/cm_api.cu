@@ -1,4 +1,5 @@
 // cm_api.cu -- the C ABI declared in include/cm.h (validation, graph upload, launch).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -69,6 +70,23 @@ constexpr int64_t kDefaultWsBytes = int64_t(96) << 20;   // two 48 MB chunks: L2
 
 namespace {
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
 size_t scan_warp_bytes(int n, bool s32) { return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * ((n + 3) & ~3); }
@@ -110,12 +128,15 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   int occ1 = 0, occ2 = 0;
-  const size_t smem1 = 0;
+  const size_t smem1 = sizeof(cm2::K1Smem);
   {
-    // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~224 KB per SM).
+    // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
+      e = cudaFuncSetAttribute(cm2::round_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(cm2::K1Smem));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -125,7 +146,23 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       carve = true;
     }
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_pack_kernel, 256, smem1);
+  const bool use_tma = a->layout == CM_LAYOUT_DENSE;
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (use_tma) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(CM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {(cuuint64_t)a->ld, (cuuint64_t)n, (cuuint64_t)a->n_sstar};
+    const cuuint64_t strides[2] = {(cuuint64_t)a->ld * 4, (cuuint64_t)a->sstar_stride * 4};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
+  }
+  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel, 256, smem1);
+  else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_ldg_kernel, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
@@ -192,7 +229,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
       rp.th0 = th0;
       rp.nt = std::min(4, a->n_theta - th0);
-      cm2::round_pack_kernel<<<grid1, 256, smem1, g->st_round>>>(rp);
+      if (use_tma) cm2::round_tma_kernel<<<grid1, 256, smem1, g->st_round>>>(rp, tmap);
+      else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
     }
     e = cudaEventRecord(g->ev_round[b], g->st_round);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_round[b], 0);

@@ -33,6 +33,7 @@
 // Layout of one candidate's column array in the workspace: group g holds nodes 0..32g+31 at
 // word offset grp_off(g) = 16 g (g+1) (16-byte aligned).
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 
 namespace cm2 {
@@ -91,14 +92,141 @@ struct RoundParams {
   int32_t brow;               // word offset of brow in a candidate block
 };
 
-// Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31 (the S_{t+1} rows of the
+// ---- bulk-async copy + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+// 3-D tensor-map TMA: box {32 nodes, 32 rows, 1 S*} at (x = node, y = row, z = S*).
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
+}
+
+// K1 for the dense layout.  Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31
+// (the S_{t+1} rows of the group's stages), 32 nodes (block w) at a time.  One elected lane
+// loads block w with a single 3-D tensor-map TMA (rows >= n are zero-filled) into a
+// 3-stage shared ring (one mbarrier per stage), two blocks ahead of the consumer.  Consumption: lane = node, one LDS + one
+// compare (a1, strict fp32 '>', NaN -> 0) + one ballot per row, which is the packed row
+// word.  The row words go through a 32-word shared slot to lane q, which transposes them
+// into column words and adds its row's checkpoint mass mass_r = sum_{i in S_r} M_i (the
+// Eq. 6 sum) from 4-bit tables.
+constexpr int kStages = 3;
+constexpr int kK1Warps = 8;
+struct K1Smem {
+  float tile[kK1Warps][kStages][32][32];
+  uint64_t bar[kK1Warps][kStages];
+  uint32_t rows_w[kK1Warps][32];
+};
+
+__global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char k1smem[];
+  K1Smem& sm = *reinterpret_cast<K1Smem*>(k1smem);
+  const int64_t* nib = p.nib;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const int tasks = p.s_count * p.G;
+  if (lane == 0)
+    for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wl][st], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+
+  // producer cursor: (task, w) sequence of this warp
+  int pt = wid, pw = 0, pstage = 0;
+  auto issue = [&]() {
+    if (pt >= tasks) return;
+    const int s = pt / p.G, g = pt - (pt / p.G) * p.G;
+    if (lane == 0) {
+      mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
+      tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * g + 1, (int)(p.s_begin + s),
+                  &sm.bar[wl][pstage]);
+    }
+    pstage = pstage + 1 == kStages ? 0 : pstage + 1;
+    if (++pw > g) { pw = 0; pt += nw; }
+  };
+  for (int d = 0; d < kStages - 1; ++d) issue();
+
+  const float qnan = __int_as_float(0x7fffffff);
+  int cstage = 0;
+  uint32_t phase[kStages] = {0u, 0u, 0u};
+  for (int task = wid; task < tasks; task += nw) {
+    const int s = task / p.G;
+    const int g = task - s * p.G;
+    uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
+    const int rq = 32 * g + lane + 1;                               // row owned by this lane
+    const bool full_rows = (32 * g + 32) < p.n;                     // every r_q exists
+    int64_t mass[4] = {0, 0, 0, 0};
+    for (int w = 0; w <= g; ++w) {
+      issue();                                                      // keep kStages-1 blocks ahead
+      mbar_wait(&sm.bar[wl][cstage], phase[cstage]);
+      phase[cstage] ^= 1u;
+      const float(*tl)[32] = sm.tile[wl][cstage];
+      const int node = 32 * w + lane;
+      float x[32];
+      if (w < g && full_rows) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int r = 32 * g + 1 + q;
+          x[q] = (r < p.n && node < r) ? tl[q][lane] : qnan;
+        }
+      }
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile reads before its reuse
+      cstage = cstage + 1 == kStages ? 0 : cstage + 1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= p.nt) break;
+        const float th = __ldg(p.theta + p.th0 + j);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) sm.rows_w[wl][q] = __ballot_sync(FULL, x[q] > th);
+        __syncwarp();
+        const uint32_t word = sm.rows_w[wl][lane];                  // row r_q's word, block w
+        __syncwarp();
+        int64_t ms = 0;
+        if (word) {
+          const int64_t* tw = nib + 128 * w;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+        }
+        uint32_t* oj = out + (int64_t)j * p.cs;
+        if (lane == 31 && g + 1 < p.G) oj[p.brow + (g + 1) * p.G + w] = word;   // row 32(g+1)
+        oj[grp_off(g) + node] = transpose32(word, lane);
+        mass[j] += ms;
+      }
+    }
+    if (rq < p.n) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+    }
+  }
+}
+
+// K1 for the packed tri4 layout (rows of irregular stride).  Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31 (the S_{t+1} rows of the
 // group's stages), 32 nodes (block w) at a time.  Lane = node: row q of the block is one
 // coalesced 128-byte load, one compare (a1, strict fp32 '>', NaN -> 0) and one ballot, which
 // is already the packed row word.  The 32 row words go through a 32-word shared slot to
 // lane q, which transposes them into column words and adds the checkpoint mass of its
 // row, mass_r = sum_{i in S_r} M_i (the Eq. 6 sum), from 4-bit tables.
 // Out-of-triangle elements are replaced by NaN, which compares false for every theta.
-__global__ void __launch_bounds__(256) round_pack_kernel(const RoundParams p) {
+__global__ void __launch_bounds__(256) round_ldg_kernel(const RoundParams p) {
   __shared__ uint32_t rows_w[8][32];                              // per-warp ballot slot
   __shared__ int64_t rows_off[8][32];                             // per-warp row offsets
   const int64_t* nib = p.nib;
@@ -217,15 +345,31 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
     }
   }
   const uint32_t selff = Rk & ~a;                                   // FREE_{t,k,k}
-  // every free at k lies in a stage that computes k: E = max(E - GC(k), 0) + M_k
-  for (uint32_t x = Rk; x; x &= x - 1) {
-    const int b = __ffs(x) - 1;
-    ET ev = E[32 * b + lane];
-    if ((selff >> b) & 1u) ev -= Mk;
+  // every free at k lies in a stage that computes k: E = max(E - GC(k), 0) + M_k.
+  // Up to four stage bits per round: their loads issue together (latency, not issue, bound).
+  for (uint32_t x = Rk; x;) {
+    int b[4];
+    bool v[4];
 #pragma unroll
-    for (int j = 0; j < ND; ++j)
-      if ((f[j] >> b) & 1u) ev -= mi[j];
-    E[32 * b + lane] = (ev > 0 ? ev : (ET)0) + Mk;
+    for (int u = 0; u < 4; ++u) {
+      v[u] = x != 0u;
+      b[u] = v[u] ? __ffs(x) - 1 : 0;
+      x &= x - 1;
+    }
+    ET ev[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ev[u] = v[u] ? E[32 * b[u] + lane] : (ET)0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((selff >> b[u]) & 1u) ev[u] -= Mk;
+#pragma unroll
+      for (int j = 0; j < ND; ++j)
+        if ((f[j] >> b[u]) & 1u) ev[u] -= mi[j];
+      ev[u] = (ev[u] > 0 ? ev[u] : (ET)0) + Mk;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v[u]) E[32 * b[u] + lane] = ev[u];
   }
 }
 
@@ -261,13 +405,25 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
     // A'_i = Sn_i | Acc_i (Acc = OR of R over visited users): the closure reads Sn_k | Acc_k and
     // every FREE test reads Sn_i | Acc_i, so one array serves both.  Start: A' = Sn.
-    for (int q = 0; q < nq; ++q) {
-      const uint4 v = live ? __ldcg(sn4 + q) : make_uint4(0u, 0u, 0u, 0u);
-      const int i0 = 4 * q;
-      A[32 * i0 + lane] = v.x;
-      if (i0 + 1 < nk) A[32 * (i0 + 1) + lane] = v.y;
-      if (i0 + 2 < nk) A[32 * (i0 + 2) + lane] = v.z;
-      if (i0 + 3 < nk) A[32 * (i0 + 3) + lane] = v.w;
+    {  // software-pipelined: the loads of 8 quads are in flight while the previous 8 are stored
+      uint4 va[8], vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) va[u] = (live && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
+      for (int q0 = 0; q0 < nq; q0 += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          vb[u] = (live && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i0 = 4 * (q0 + u);
+          if (i0 + 0 < nk) A[32 * (i0 + 0) + lane] = va[u].x;
+          if (i0 + 1 < nk) A[32 * (i0 + 1) + lane] = va[u].y;
+          if (i0 + 2 < nk) A[32 * (i0 + 2) + lane] = va[u].z;
+          if (i0 + 3 < nk) A[32 * (i0 + 3) + lane] = va[u].w;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) va[u] = vb[u];
+      }
     }
     for (int b = 0; b < 32; ++b) E[32 * b + lane] = (ET)0;
     __syncwarp();
@@ -275,9 +431,17 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     int64_t costL = 0;
     uint4 cur = live ? __ldcg(sn4 + nq - 1) : make_uint4(0u, 0u, 0u, 0u);
     uint32_t a_next = A[32 * (nk - 1) + lane];
+    // row 32g's word for the current 32-node block; the next block's word is prefetched
+    uint32_t bword = (g > 0 && ((nq - 1) >> 3) < g && live) ? brow[(nq - 1) >> 3] : 0u;
+    uint32_t bnext = (g > 0 && ((nq - 1) >> 3) >= 1 && ((nq - 1) >> 3) - 1 < g && live)
+                         ? brow[((nq - 1) >> 3) - 1] : 0u;
     for (int q = nq - 1; q >= 0; --q) {
       const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t bword = (g > 0 && (q >> 3) < g && live) ? brow[q >> 3] : 0u;
+      if ((q & 7) == 7 && q != nq - 1) {                            // entered a new 32-node block
+        bword = bnext;
+        const int wb = (q >> 3) - 1;
+        bnext = (g > 0 && wb >= 0 && wb < g && live) ? brow[wb] : 0u;
+      }
 #pragma unroll
       for (int u = 3; u >= 0; --u) {
         const int k = 4 * q + u;
@@ -304,12 +468,16 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     }
     // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
     const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
-    int64_t pk = INT64_MIN;
-    for (int b = 0; b < 32 && 32 * g + b < n; ++b) {
+    int64_t mv[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {                                  // issue all 32 loads first
       const int r = 32 * g + b;
-      const int64_t m = (r && live) ? __ldcg(mass + r) : 0;
-      pk = max(pk, m + (int64_t)E[32 * b + lane]);
+      mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
     }
+    int64_t pk = INT64_MIN;
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+      if (32 * g + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * b + lane]);
     if (live) {
       int64_t* pp = p.part + 2 * (c * G + g);
       pp[0] = pk;
