@@ -453,6 +453,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
         const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
         const uint32_t Rk = (a & ~sw) | diag;                       // a2 seed + a3 closure
         A[32 * k + lane] = Rk;                                      // slot now holds R column
+        if (!__any_sync(FULL, Rk != 0u)) continue;                  // k computed in no lane: no pushes,
+                                                                    // frees or allocations
         const ET Mk = (ET)M[k];
         costL += (int64_t)__popc(Rk) * C[k];
         const int e0 = pred_ptr[k], nd = pred_ptr[k + 1] - e0;

@@ -1,0 +1,117 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the cross-rank argmin (a8): contiguous
+S* shards with global candidate indices, packed (cost << idx_bits | idx) keys, all-reduce
+MIN.  The per-candidate results come from the CPU oracle; the reduction under test is
+paper_1910_02653_b200.dist (no CUDA needed)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+KEY_NONE = (1 << 63) - 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _keys_for(peaks, costs, budgets, index_base, idx_bits):
+    keys = []
+    for b in budgets:
+        best = KEY_NONE
+        for c, (p, q) in enumerate(zip(peaks, costs)):
+            if p <= b:
+                best = min(best, (q << idx_bits) | (index_base + c))
+        keys.append(best)
+    return keys
+
+
+def _worker(rank, world, port, n_sstar, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import importlib.util
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        spec = importlib.util.spec_from_file_location("cm_dist", os.path.join(root, "paper_1910_02653_b200", "dist.py"))
+        D = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(D)
+        from oracle import Instance, evaluate
+        from workloads import budgets as B
+        from workloads import graphs as G
+        from workloads.sstar import gen_sstar
+        g = G.random_training(6, 0.2, 3)
+        inst = Instance.from_graph(g)
+        budgets = list(B.geometric_grid(g, 6))
+        lo, hi = D.shard_range(n_sstar, rank, world)
+        thetas = [0.5, 0.6]
+        total = n_sstar * len(thetas)
+        idx_bits = max(1, (total - 1).bit_length())
+        peaks, costs = [], []
+        for s in range(lo, hi):
+            x = gen_sstar(g, "mix", 17, s, 1)[0]
+            for th in thetas:
+                o = evaluate(inst, x, th)
+                peaks.append(o["peak"])
+                costs.append(o["cost"])
+        keys = torch.tensor(_keys_for(peaks, costs, budgets, lo * len(thetas), idx_bits), dtype=torch.int64)
+        D.global_best(keys)
+        if rank == 0:
+            out_q.put((keys.tolist(), D.decode_keys(keys, idx_bits), idx_bits))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_sstar", [5, 8])
+def test_global_best_two_ranks(n_sstar):
+    from oracle import Instance, best_per_budget, evaluate
+    from workloads import budgets as B
+    from workloads import graphs as G
+    from workloads.sstar import gen_sstar
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_sstar, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    keys, decoded, idx_bits = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single-process reference over all candidates
+    g = G.random_training(6, 0.2, 3)
+    inst = Instance.from_graph(g)
+    budgets = list(B.geometric_grid(g, 6))
+    peaks, costs = [], []
+    for s in range(n_sstar):
+        x = gen_sstar(g, "mix", 17, s, 1)[0]
+        for th in [0.5, 0.6]:
+            o = evaluate(inst, x, th)
+            peaks.append(o["peak"])
+            costs.append(o["cost"])
+    want = best_per_budget(peaks, costs, budgets)
+    for (widx, wcost), (cost, idx) in zip(want, decoded):
+        if widx < 0:
+            assert (cost, idx) == (-1, -1)
+        else:
+            assert (cost, idx) == (wcost, widx)
+
+
+def test_shard_ranges_cover():
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("cm_dist", os.path.join(root, "paper_1910_02653_b200", "dist.py"))
+    D = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(D)
+    for N in [0, 1, 7, 125000, 10 ** 6]:
+        for P in [1, 2, 3, 8]:
+            rs = [D.shard_range(N, r, P) for r in range(P)]
+            assert rs[0][0] == 0 and rs[-1][1] == N
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(P - 1))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
