@@ -89,7 +89,14 @@ EncodeTiledFn encode_tiled() {
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
-size_t scan_warp_bytes(int n, bool s32) { return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * ((n + 3) & ~3); }
+size_t scan_warp_bytes(int n, bool s32, bool tm) {
+  const int spill = std::max(0, ((n + 3) & ~3) - (tm ? 256 : 0));   // A' nodes kept in shared memory
+  return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * spill;
+}
+bool tmem_enabled() {
+  const char* e = std::getenv("CM_TMEM");
+  return !(e && std::strcmp(e, "0") == 0);
+}
 
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
@@ -104,13 +111,17 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   if (cap < std::max<int64_t>(32, a->n_theta)) return fail(CM_EINVAL, "workspace too small");
   const int64_t chunk_s = std::min<int64_t>(cap / a->n_theta, 1 << 20);   // S* per chunk
 
-  const size_t wb = scan_warp_bytes(n, g->scan32);
-  const void* scan_fn = g->scan32 ? reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>)
-                                  : reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>);
+  // Scan kernel variant: A' in Tensor Memory (+ shared spill) with 8 warps per SM when that
+  // fits, else all in shared memory with as many warps as fit.
   const size_t fixed = (size_t)g->blob2_bytes;
+  const bool tm = tmem_enabled() && fixed + 8 * scan_warp_bytes(n, g->scan32, true) + 1024 <= (size_t)g->smem_optin;
+  const size_t wb = scan_warp_bytes(n, g->scan32, tm);
   if (fixed + wb > (size_t)g->smem_optin) return fail(CM_ERANGE, "scan kernel: shared memory exceeded");
-  const int wpc = (int)std::min<size_t>(8, ((size_t)g->smem_optin - fixed) / wb);
+  const int wpc = tm ? 8 : (int)std::min<size_t>(8, ((size_t)g->smem_optin - fixed) / wb);
   const size_t smem2 = fixed + wb * wpc;
+  const void* scan_fn = g->scan32
+      ? (tm ? reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>) : reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>))
+      : (tm ? reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>) : reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>));
 
   static std::mutex attr_mu;
   static size_t set2 = 0;
@@ -118,8 +129,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   {
     std::lock_guard<std::mutex> lock(attr_mu);
     if (smem2 > set2) {
-      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>),
-                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>)}) {
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(smem2, 48 * 1024));
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(scan_kernel)");
@@ -137,8 +150,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       e = cudaFuncSetAttribute(cm2::round_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)sizeof(cm2::K1Smem));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
-      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t>),
-                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t>)}) {
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
@@ -241,9 +256,16 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     sp.part = part;
     sp.out_base = s0 * a->n_theta;
     const int64_t tasks = (int64_t)G * sp.n_batch;
-    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + wpc - 1) / wpc, (int64_t)occ2 * g->sm_count));
-    if (g->scan32) cm2::scan_kernel<int32_t><<<grid2, 32 * wpc, smem2, st>>>(sp);
-    else cm2::scan_kernel<int64_t><<<grid2, 32 * wpc, smem2, st>>>(sp);
+    // TM: one CTA per SM (each allocates all 512 TMEM columns)
+    const int64_t max_ctas = tm ? (int64_t)g->sm_count : (int64_t)occ2 * g->sm_count;
+    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + wpc - 1) / wpc, max_ctas));
+    if (g->scan32) {
+      if (tm) cm2::scan_kernel<int32_t, true><<<grid2, 32 * wpc, smem2, st>>>(sp);
+      else cm2::scan_kernel<int32_t, false><<<grid2, 32 * wpc, smem2, st>>>(sp);
+    } else {
+      if (tm) cm2::scan_kernel<int64_t, true><<<grid2, 32 * wpc, smem2, st>>>(sp);
+      else cm2::scan_kernel<int64_t, false><<<grid2, 32 * wpc, smem2, st>>>(sp);
+    }
     qp.part = part;
     qp.n_cand = nc;
     qp.out_base = sp.out_base;
@@ -510,7 +532,7 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
   if (n_cand == 0) return CM_OK;
-  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n, g->scan32) <= (size_t)g->smem_optin) {
+  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n, g->scan32, false) <= (size_t)g->smem_optin) {
     cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);

@@ -313,12 +313,54 @@ struct ScanParams {
   int32_t warp_bytes;         // shared bytes per warp region
 };
 
+// A' storage of one warp.  TM = false: shared memory [node][lane].  TM = true: nodes < tmc
+// live in Tensor Memory -- lane = TMEM lane (this warp's 32-lane quarter), node = TMEM
+// column, accessed with tcgen05.ld/st.32x32b (one column, all 32 lanes, uniform address)
+// -- and nodes >= tmc spill to shared memory.  Stores are made visible to later loads by
+// tcgen05.wait::st, issued once per node step (fence_st).
+template <bool TM>
+struct AView {
+  uint32_t* sm;
+  uint32_t taddr;
+  int tmc;
+  int lane;
+  __device__ __forceinline__ uint32_t ld(int k) const {
+    if (TM && k < tmc) {
+      uint32_t v;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)k) : "memory");
+      asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
+      return v;
+    }
+    return sm[32 * (k - tmc) + lane];
+  }
+  __device__ __forceinline__ void st(int k, uint32_t v) const {
+    if (TM && k < tmc)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)k), "r"(v) : "memory");
+    else
+      sm[32 * (k - tmc) + lane] = v;
+  }
+  __device__ __forceinline__ void st4(int k, uint4 v) const {   // nodes k..k+3, k % 4 == 0
+    if (TM && k < tmc)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+                   :: "r"(taddr + (uint32_t)k), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    else {
+      sm[32 * (k + 0 - tmc) + lane] = v.x;
+      sm[32 * (k + 1 - tmc) + lane] = v.y;
+      sm[32 * (k + 2 - tmc) + lane] = v.z;
+      sm[32 * (k + 3 - tmc) + lane] = v.w;
+    }
+  }
+  __device__ __forceinline__ void fence_st() const {
+    if (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+};
+
 // One node k of the group-g pass for dependency count ND (0..4; ND = 4 also walks any
 // further dependencies).  Specialised so the event loop carries exactly ND free masks.
-template <int ND, typename ET>
+template <int ND, typename ET, bool TM>
 __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk, int e0, int nd,
                                           const int32_t* __restrict__ pred_idx,
-                                          const int64_t* __restrict__ M, uint32_t* A, ET* E,
+                                          const int64_t* __restrict__ M, const AView<TM>& A, ET* E,
                                           int lane, uint32_t& a_next) {
   uint32_t f[ND > 0 ? ND : 1];
   ET mi[ND > 0 ? ND : 1];
@@ -326,9 +368,9 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
   for (int j = 0; j < ND; ++j) {                                   // FREE_{t,i,k} = R_k & ~A'_i
     const int i = pred_idx[e0 + j];
     const bool nb = (i == k - 1);
-    const uint32_t ai = nb ? a_next : A[32 * i + lane];
+    const uint32_t ai = nb ? a_next : A.ld(i);
     f[j] = Rk & ~ai;
-    A[32 * i + lane] = ai | Rk;                                     // A'_i |= R_k
+    A.st(i, ai | Rk);                                               // A'_i |= R_k
     if (nb) a_next = ai | Rk;
     mi[j] = (ET)M[i];
   }
@@ -336,9 +378,9 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
     for (int e = e0 + 4; e < e0 + nd; ++e) {                       // in-degree > 4 (rare)
       const int i = pred_idx[e];
       const bool nb = (i == k - 1);
-      const uint32_t ai = nb ? a_next : A[32 * i + lane];
+      const uint32_t ai = nb ? a_next : A.ld(i);
       uint32_t fx = Rk & ~ai;
-      A[32 * i + lane] = ai | Rk;
+      A.st(i, ai | Rk);
       if (nb) a_next = ai | Rk;
       const ET Mi = (ET)M[i];
       for (; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
@@ -375,8 +417,10 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
 
 // ET = int32_t when every M is a multiple of a scale s with sum M/s < 2^30 (the host checks;
 // exact), else int64_t.  M in the blob, the masses and the results are in units of s.
-template <typename ET>
-__global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
+// TM: A' of nodes < 256 in Tensor Memory (8 warps, one CTA per SM, 512 TMEM columns:
+// warp w uses lane quarter w % 4 and columns 256 * (w / 4) ..).
+template <typename ET, bool TM>
+__global__ void __launch_bounds__(256, 1) scan_kernel(const ScanParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = p.n, G = p.G;
@@ -387,10 +431,23 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
   const int32_t* pred_idx = gi + p.o_pred_idx;
   unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
   ET* E = reinterpret_cast<ET*>(wr);                               // [32 stages][32 lanes]
-  uint32_t* A = reinterpret_cast<uint32_t*>(E + 32 * 32);           // [node][lane]: Sn | Acc, then R
+  uint32_t* Asm = reinterpret_cast<uint32_t*>(E + 32 * 32);         // [node][lane] (spill part)
+  __shared__ uint32_t tmem_base;
   for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_base)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  AView<TM> A;
+  A.sm = Asm;
+  A.lane = lane;
+  A.tmc = TM ? min(p.n, 256) : 0;
+  A.taddr = TM ? tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2) : 0u;
 
   const int tasks = G * p.n_batch;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -416,10 +473,14 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i0 = 4 * (q0 + u);
-          if (i0 + 0 < nk) A[32 * (i0 + 0) + lane] = va[u].x;
-          if (i0 + 1 < nk) A[32 * (i0 + 1) + lane] = va[u].y;
-          if (i0 + 2 < nk) A[32 * (i0 + 2) + lane] = va[u].z;
-          if (i0 + 3 < nk) A[32 * (i0 + 3) + lane] = va[u].w;
+          if (i0 >= nk) break;                                      // warp-uniform
+          if (TM && i0 < A.tmc) A.st4(i0, va[u]);                   // tmc % 4 == 0 or tmc == n
+          else {
+            if (i0 + 0 < nk) A.st(i0 + 0, va[u].x);
+            if (i0 + 1 < nk) A.st(i0 + 1, va[u].y);
+            if (i0 + 2 < nk) A.st(i0 + 2, va[u].z);
+            if (i0 + 3 < nk) A.st(i0 + 3, va[u].w);
+          }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) va[u] = vb[u];
@@ -430,7 +491,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
     int64_t costL = 0;
     uint4 cur = live ? __ldcg(sn4 + nq - 1) : make_uint4(0u, 0u, 0u, 0u);
-    uint32_t a_next = A[32 * (nk - 1) + lane];
+    A.fence_st();
+    uint32_t a_next = A.ld(nk - 1);
     // row 32g's word for the current 32-node block; the next block's word is prefetched
     uint32_t bword = (g > 0 && ((nq - 1) >> 3) < g && live) ? brow[(nq - 1) >> 3] : 0u;
     uint32_t bnext = (g > 0 && ((nq - 1) >> 3) >= 1 && ((nq - 1) >> 3) - 1 < g && live)
@@ -448,22 +510,23 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
         if (k >= nk) continue;                                      // warp-uniform
         const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
         const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);  // S_t from S_{t+1} and row 32g
+        A.fence_st();                                               // earlier stores visible
         const uint32_t a = a_next;                                  // A'_k = Sn_k | Acc_k (complete)
-        a_next = k > 0 ? A[32 * (k - 1) + lane] : 0u;               // prefetch; fixed up on a push
+        a_next = k > 0 ? A.ld(k - 1) : 0u;                          // prefetch; fixed up on a push
         const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
         const uint32_t Rk = (a & ~sw) | diag;                       // a2 seed + a3 closure
-        A[32 * k + lane] = Rk;                                      // slot now holds R column
+        A.st(k, Rk);                                                // slot now holds R column
         if (!__any_sync(FULL, Rk != 0u)) continue;                  // k computed in no lane: no pushes,
                                                                     // frees or allocations
         const ET Mk = (ET)M[k];
         costL += (int64_t)__popc(Rk) * C[k];
         const int e0 = pred_ptr[k], nd = pred_ptr[k + 1] - e0;
         switch (nd) {                                               // warp-uniform
-          case 0: node_step<0, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 1: node_step<1, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 2: node_step<2, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 3: node_step<3, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          default: node_step<4, ET>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 0: node_step<0, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 1: node_step<1, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 2: node_step<2, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          case 3: node_step<3, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
+          default: node_step<4, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
         }
       }
       cur = nxt;
@@ -486,33 +549,55 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
       pp[1] = costL;
     }
     if (p.r_mask32 || p.s_mask32) {                                 // verification output
+      A.fence_st();
       __syncwarp();
       const int W32 = 2 * ((n + 63) >> 6);
+      uint32_t* scratch = reinterpret_cast<uint32_t*>(E);             // E is dead: [32 nodes][32 lanes]
+      for (int w = 0; w <= g; ++w) {
+        for (int j = 0; j < 32; ++j) {
+          const int node = 32 * w + j;
+          scratch[32 * j + lane] = node < nk ? A.ld(node) : 0u;      // R column, own candidate
+        }
+        __syncwarp();
+        for (int cl = 0; cl < 32; ++cl) {
+          const int64_t cc = (int64_t)(task % p.n_batch) * 32 + cl;
+          if (cc >= p.n_cand) break;                                // warp-uniform
+          const uint32_t* ccw = p.ws + cc * p.cs;
+          const int row = 32 * g + lane;
+          const int node = 32 * w + lane;
+          const uint32_t rc = scratch[32 * lane + cl];
+          uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
+          const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
+          sc = (sc << 1) | ((bb >> lane) & 1u);
+          const uint32_t xr = transpose32(rc, lane);
+          const uint32_t xs = transpose32(sc, lane);
+          if (row < n) {
+            const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32;
+            if (p.r_mask32) p.r_mask32[o + w] = xr;
+            if (p.s_mask32) p.s_mask32[o + w] = xs;
+          }
+        }
+        __syncwarp();
+      }
+      const int row = 32 * g + lane;                                // zero the words above the block diagonal
       for (int cl = 0; cl < 32; ++cl) {
         const int64_t cc = (int64_t)(task % p.n_batch) * 32 + cl;
-        if (cc >= p.n_cand) break;                                  // warp-uniform
-        const uint32_t* ccw = p.ws + cc * p.cs;
-        const int row = 32 * g + lane;
-        for (int w = 0; w < W32; ++w) {
-          uint32_t xr = 0, xs = 0;
-          if (w <= g) {
-            const int node = 32 * w + lane;
-            const uint32_t rc = node < nk ? A[32 * node + cl] : 0u;
-            uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
-            const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
-            sc = (sc << 1) | ((bb >> lane) & 1u);
-            xr = transpose32(rc, lane);
-            xs = transpose32(sc, lane);
-          }
-          if (row < n) {
-            const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32 + w;
-            if (p.r_mask32) p.r_mask32[o] = xr;
-            if (p.s_mask32) p.s_mask32[o] = xs;
-          }
+        if (cc >= p.n_cand || row >= n) break;
+        const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32;
+        for (int w = g + 1; w < W32; ++w) {
+          if (p.r_mask32) p.r_mask32[o + w] = 0u;
+          if (p.s_mask32) p.s_mask32[o + w] = 0u;
         }
       }
     }
     __syncwarp();
+  }
+  if (TM) {
+    A.fence_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem_base) : "memory");
   }
 }
 
