@@ -114,6 +114,12 @@ int32_t cm_key_idx_bits(int64_t total_candidates);
 /* key -> (cost, idx); key == CM_KEY_NONE -> cost = -1, idx = -1. */
 void cm_decode_key(int64_t key, int32_t idx_bits, int64_t* cost, int64_t* idx);
 
+/* Debug aid: with the environment variable CM_TRACE=1, cm_round_and_evaluate records CUDA
+ * events around each internal chunk's rounding (K1) and scan (K2+K3) launches; after that
+ * call completed, this writes (k1_begin, k1_end, k2_begin, k2_end) per chunk, in ms relative
+ * to the first k1_begin, into out[max_values] and returns the count written (0 if none). */
+int32_t cm_debug_trace(float* out, int32_t max_values);
+
 const char* cm_status_string(cm_status s);
 const char* cm_last_error(void);
 

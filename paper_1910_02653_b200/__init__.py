@@ -96,6 +96,13 @@ def decode_key(key: int, idx_bits: int):
     return int(c.value), int(i.value)
 
 
+def debug_trace(max_values: int = 4096):
+    """(k1_begin, k1_end, k2_begin, k2_end) per chunk of the last CM_TRACE=1 call, in ms."""
+    buf = (ctypes.c_float * max_values)()
+    m = _lib.cm_debug_trace(buf, max_values)
+    return [tuple(buf[i:i + 4]) for i in range(0, m, 4)]
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 

@@ -64,7 +64,7 @@ int cpw_override() {
   const char* e = std::getenv("CM_CPW");
   return e ? std::atoi(e) : 0;
 }
-constexpr int64_t kDefaultWsBytes = int64_t(96) << 20;   // two 48 MB chunks: L2-resident (126 MB L2)
+constexpr int64_t kDefaultWsBytes = int64_t(256) << 20;  // two 128 MB chunk buffers: >= 3 waves of scan tasks
 }  // namespace
 
 
@@ -93,6 +93,27 @@ size_t scan_warp_bytes(int n, bool s32, bool tm) {
   const int spill = std::max(0, ((n + 3) & ~3) - (tm ? 256 : 0));   // A' nodes kept in shared memory
   return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * spill;
 }
+// CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
+// launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).
+struct Trace {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // per chunk: k1 begin, k1 end, k2 begin, k2 end
+  int used = 0;
+};
+Trace g_trace;
+bool trace_enabled() {
+  const char* e = std::getenv("CM_TRACE");
+  return e && std::strcmp(e, "1") == 0;
+}
+cudaEvent_t trace_event(int i) {
+  while ((int)g_trace.ev.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_trace.ev.push_back(e);
+  }
+  return g_trace.ev[i];
+}
+
 bool tmem_enabled() {
   const char* e = std::getenv("CM_TMEM");
   return !(e && std::strcmp(e, "0") == 0);
@@ -153,7 +174,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
-                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>)}) {
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel),
+                             reinterpret_cast<const void*>(cm2::round_ldg_kernel)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
@@ -225,6 +248,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   const int64_t half = cap * cand_bytes(n);
   std::lock_guard<std::mutex> lock(g->mu);
+  const bool tr = trace_enabled();
+  g_trace.used = 0;
   e = cudaEventRecord(g->ev_start, st);                       // inputs written on `st` before the call
   if (e == cudaSuccess) e = cudaStreamWaitEvent(g->st_round, g->ev_start, 0);
   int c = 0;
@@ -240,16 +265,21 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     rp.s_count = sc;
     rp.sn = blk;
     const int64_t warps1 = (int64_t)sc * G;
-    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + 7) / 8, (int64_t)occ1 * g->sm_count));
+    // one K1 CTA per SM (8 warps, 64 KB, 32k registers): it co-resides with the scan CTA
+    // (TMEM variant: 8 warps, ~144 KB, 32k registers), so chunk c+1 streams while c scans.
+    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + 7) / 8, (int64_t)g->sm_count));
+    if (tr) cudaEventRecord(trace_event(4 * c + 0), g->st_round);
     for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
       rp.th0 = th0;
       rp.nt = std::min(4, a->n_theta - th0);
       if (use_tma) cm2::round_tma_kernel<<<grid1, 256, smem1, g->st_round>>>(rp, tmap);
       else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
     }
+    if (tr) cudaEventRecord(trace_event(4 * c + 1), g->st_round);
     e = cudaEventRecord(g->ev_round[b], g->st_round);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_round[b], 0);
     if (e != cudaSuccess) break;
+    if (tr) cudaEventRecord(trace_event(4 * c + 2), st);
     sp.ws = blk;
     sp.n_cand = nc;
     sp.n_batch = (int)((nc + 31) / 32);
@@ -270,6 +300,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     qp.n_cand = nc;
     qp.out_base = sp.out_base;
     cm2::reduce_kernel<<<(int)((nc + 255) / 256), 256, 0, st>>>(qp);
+    if (tr) {
+      cudaEventRecord(trace_event(4 * c + 3), st);
+      g_trace.used = 4 * (c + 1);
+    }
     e = cudaEventRecord(g->ev_scan[b], st);
     g->used[b] = true;
   }
@@ -493,6 +527,20 @@ void cm_graph_destroy(cm_graph* g) {
   if (g->d_ws) cudaFree(g->d_ws);
   if (g->d_nib) cudaFree(g->d_nib);
   delete g;
+}
+
+// Debug: after a CM_TRACE=1 call has completed, writes per-chunk (k1_begin, k1_end,
+// k2_begin, k2_end) in ms relative to the first k1_begin; returns the number of values.
+int32_t cm_debug_trace(float* out, int32_t max_values) {
+  int32_t m = 0;
+  if (g_trace.used == 0) return 0;
+  cudaEventSynchronize(g_trace.ev[g_trace.used - 1]);
+  for (int i = 0; i < g_trace.used && m < max_values; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_trace.ev[0], g_trace.ev[i]);
+    out[m++] = ms;
+  }
+  return m;
 }
 
 int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {

@@ -124,7 +124,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, 
 // word.  The row words go through a 32-word shared slot to lane q, which transposes them
 // into column words and adds its row's checkpoint mass mass_r = sum_{i in S_r} M_i (the
 // Eq. 6 sum) from 4-bit tables.
-constexpr int kStages = 3;
+constexpr int kStages = 2;     // 64 KB per CTA: co-resides with the TMEM scan CTA (144 KB)
 constexpr int kK1Warps = 8;
 struct K1Smem {
   float tile[kK1Warps][kStages][32][32];
@@ -145,24 +145,29 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
 
-  // producer cursor: (task, w) sequence of this warp
+  // producer cursor: (task, w) sequence of this warp; (ps, pg) decoded once per task
   int pt = wid, pw = 0, pstage = 0;
+  int ps = pt / p.G, pg = pt - ps * p.G;
   auto issue = [&]() {
     if (pt >= tasks) return;
-    const int s = pt / p.G, g = pt - (pt / p.G) * p.G;
     if (lane == 0) {
       mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
-      tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * g + 1, (int)(p.s_begin + s),
+      tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
                   &sm.bar[wl][pstage]);
     }
     pstage = pstage + 1 == kStages ? 0 : pstage + 1;
-    if (++pw > g) { pw = 0; pt += nw; }
+    if (++pw > pg) {
+      pw = 0;
+      pt += nw;
+      ps = pt / p.G;
+      pg = pt - ps * p.G;
+    }
   };
   for (int d = 0; d < kStages - 1; ++d) issue();
 
   const float qnan = __int_as_float(0x7fffffff);
   int cstage = 0;
-  uint32_t phase[kStages] = {0u, 0u, 0u};
+  uint32_t phase[kStages] = {};
   for (int task = wid; task < tasks; task += nw) {
     const int s = task / p.G;
     const int g = task - s * p.G;
@@ -420,7 +425,7 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
 // TM: A' of nodes < 256 in Tensor Memory (8 warps, one CTA per SM, 512 TMEM columns:
 // warp w uses lane quarter w % 4 and columns 256 * (w / 4) ..).
 template <typename ET, bool TM>
-__global__ void __launch_bounds__(256, 1) scan_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   // <= 128 regs: co-resides with K1
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = p.n, G = p.G;
