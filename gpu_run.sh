@@ -1,2 +1,5 @@
-python tools/trace_chunks.py > gpurun_out/trace.log 2>&1
-CM_TMEM=0 python tools/trace_chunks.py > gpurun_out/trace_tm0.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --batch 32768 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"scan_kernel|round_" -c 2 -o gpurun_out/prof20 python bench.py --steps 1 --warmup 0 --batch 12000 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1

@@ -39,11 +39,13 @@ struct cm_graph {
   int32_t o_pred_ptr = 0, o_pred_idx = 0, o_later = 0, o_succ_ptr = 0, o_succ_idx = 0;
   void* d_blob = nullptr;
   // v2 (stage-sliced) path
-  int32_t blob2_bytes = 0;            // M/mscale, C, pred_ptr, pred_idx only
+  int32_t blob2_bytes = 0;            // M/mscale, C, pred_ptr, pred_idx, node/dep records
+  int32_t o_nrec = 0, o_drec = 0;
   int64_t mscale = 1;                 // gcd of all M (>= 1); the scan works in units of it
   bool scan32 = false;                // sum M / mscale < 2^30: int32 per-stage state
   void* d_blob2 = nullptr;
   void* d_nib = nullptr;              // K1 nibble tables of M (checkpoint mass, Eq. 6)
+  void* d_nib32 = nullptr;            // int32 copy when scan32 (every row mass < 2^30)
   int32_t nib_entries = 0;
   void* d_ws = nullptr;               // default workspace: two chunk buffers of Sn columns
   int64_t ws_bytes = 0;
@@ -217,6 +219,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   rp.bw = cm2::block_words(G);
   rp.cs = cs;
   rp.nib = reinterpret_cast<const int64_t*>(g->d_nib);
+  rp.nib32 = reinterpret_cast<const int32_t*>(g->d_nib32);
   rp.nib_entries = g->nib_entries;
   rp.brow = cm2::brow_off(n);
 
@@ -226,6 +229,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   sp.n = n;
   sp.o_pred_ptr = 0;
   sp.o_pred_idx = n + 1;
+  sp.o_nrec = g->o_nrec;
+  sp.o_drec = g->o_drec;
   sp.cs = cs;
   sp.G = G;
   sp.brow = cm2::brow_off(n);
@@ -471,12 +476,29 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     g->scan32 = tot < (int64_t(1) << 30);
     if (!g->scan32) g->mscale = 1;
   }
-  size_t bytes2 = 16 * (size_t)n + 4 * (size_t)(n + 1 + E);
-  bytes2 = (bytes2 + 15) & ~size_t(15);
+  // + node records {(int32) M_k, e0, nd, 0} and dependency records {i, (int32) M_i}
+  size_t base2 = (16 * (size_t)n + 4 * (size_t)(n + 1 + E) + 15) & ~size_t(15);
+  g->o_nrec = (int32_t)base2;
+  g->o_drec = (int32_t)(base2 + 16 * (size_t)n);
+  size_t bytes2 = (base2 + 16 * (size_t)n + 8 * (size_t)E + 15) & ~size_t(15);
   g->blob2_bytes = (int32_t)bytes2;
   std::vector<unsigned char> blob2(bytes2, 0);
   std::memcpy(blob2.data(), blob.data(), 16 * (size_t)n + 4 * (size_t)(n + 1 + E));
   for (int i = 0; i < n; ++i) reinterpret_cast<int64_t*>(blob2.data())[i] = mem[i] / g->mscale;
+  {
+    int32_t* nr = reinterpret_cast<int32_t*>(blob2.data() + g->o_nrec);
+    int32_t* dr = reinterpret_cast<int32_t*>(blob2.data() + g->o_drec);
+    for (int k = 0; k < n; ++k) {
+      nr[4 * k + 0] = (int32_t)(mem[k] / g->mscale);      // meaningful when scan32
+      nr[4 * k + 1] = pred_ptr[k];
+      nr[4 * k + 2] = pred_ptr[k + 1] - pred_ptr[k];
+      nr[4 * k + 3] = 0;
+      for (int e = pred_ptr[k]; e < pred_ptr[k + 1]; ++e) {
+        dr[2 * e + 0] = pidx[e];
+        dr[2 * e + 1] = (int32_t)(mem[pidx[e]] / g->mscale);
+      }
+    }
+  }
   e = cudaMalloc(&g->d_blob2, bytes2);
   if (e == cudaSuccess) e = cudaMemcpy(g->d_blob2, blob2.data(), bytes2, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
@@ -488,6 +510,13 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
           if ((v >> j) & 1 && 4 * q + j < n) nib[16 * q + v] += mem[4 * q + j] / g->mscale;
     e = cudaMalloc(&g->d_nib, 8 * (size_t)g->nib_entries);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_nib, nib.data(), 8 * (size_t)g->nib_entries, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && g->scan32) {
+      std::vector<int32_t> nib32(g->nib_entries);
+      for (int i = 0; i < g->nib_entries; ++i) nib32[i] = (int32_t)nib[i];
+      e = cudaMalloc(&g->d_nib32, 4 * (size_t)g->nib_entries);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_nib32, nib32.data(), 4 * (size_t)g->nib_entries, cudaMemcpyHostToDevice);
+    }
   }
   if (e == cudaSuccess) {
     const int64_t per = cand_bytes(n);
@@ -505,6 +534,7 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     if (g->d_blob2) cudaFree(g->d_blob2);
     if (g->d_ws) cudaFree(g->d_ws);
     if (g->d_nib) cudaFree(g->d_nib);
+    if (g->d_nib32) cudaFree(g->d_nib32);
     cudaFree(g->d_blob);
     delete g;
     return fail(CM_ENOMEM, std::string("cm_graph_create: ") + cudaGetErrorString(e));
@@ -526,6 +556,7 @@ void cm_graph_destroy(cm_graph* g) {
   if (g->d_blob2) cudaFree(g->d_blob2);
   if (g->d_ws) cudaFree(g->d_ws);
   if (g->d_nib) cudaFree(g->d_nib);
+  if (g->d_nib32) cudaFree(g->d_nib32);
   delete g;
 }
 

@@ -88,6 +88,7 @@ struct RoundParams {
   int32_t cs;                 //   [Sn columns: bw words][mass: n int64]
   int32_t bw;
   const int64_t* nib;         // nibble tables: nib[p*16 + v] = sum_{j<4, bit j of v} M[4p + j]
+  const int32_t* nib32;       // the same in int32 when every row mass fits (else nullptr)
   int32_t nib_entries;        // 128 * G
   int32_t brow;               // word offset of brow in a candidate block
 };
@@ -135,7 +136,6 @@ struct K1Smem {
 __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char k1smem[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(k1smem);
-  const int64_t* nib = p.nib;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
   auto issue = [&]() {
     if (pt >= tasks) return;
     if (lane == 0) {
+      // the warp's generic reads of this stage (a previous block) precede the async write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
       tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
                   &sm.bar[wl][pstage]);
@@ -165,36 +167,30 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
   };
   for (int d = 0; d < kStages - 1; ++d) issue();
 
-  const float qnan = __int_as_float(0x7fffffff);
   int cstage = 0;
-  uint32_t phase[kStages] = {};
+  uint32_t phase_bits = 0u;                                         // bit st = parity of stage st
   for (int task = wid; task < tasks; task += nw) {
     const int s = task / p.G;
     const int g = task - s * p.G;
     uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
     const int rq = 32 * g + lane + 1;                               // row owned by this lane
-    const bool full_rows = (32 * g + 32) < p.n;                     // every r_q exists
     int64_t mass[4] = {0, 0, 0, 0};
     for (int w = 0; w <= g; ++w) {
       issue();                                                      // keep kStages-1 blocks ahead
-      mbar_wait(&sm.bar[wl][cstage], phase[cstage]);
-      phase[cstage] ^= 1u;
+      mbar_wait(&sm.bar[wl][cstage], (phase_bits >> cstage) & 1u);
+      phase_bits ^= 1u << cstage;
       const float(*tl)[32] = sm.tile[wl][cstage];
-      const int node = 32 * w + lane;
       float x[32];
-      if (w < g && full_rows) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int r = 32 * g + 1 + q;
-          x[q] = (r < p.n && node < r) ? tl[q][lane] : qnan;
-        }
-      }
-      __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile reads before its reuse
+      for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
+      __syncwarp();                                                 // all lanes read the tile
       cstage = cstage + 1 == kStages ? 0 : cstage + 1;
+      // Row-word mask of this lane's row: nodes i < rq of block w (strict lower triangle) and
+      // rq < n.  Masking the row words masks the transposed columns too; zero-filled or
+      // upper-triangle tile entries never leak.
+      const int cnt = rq < p.n ? min(max(rq - 32 * w, 0), 32) : 0;
+      const uint32_t rmask = cnt >= 32 ? FULL : ((1u << cnt) - 1u);
+      const int node = 32 * w + lane;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j >= p.nt) break;
@@ -202,13 +198,21 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
 #pragma unroll
         for (int q = 0; q < 32; ++q) sm.rows_w[wl][q] = __ballot_sync(FULL, x[q] > th);
         __syncwarp();
-        const uint32_t word = sm.rows_w[wl][lane];                  // row r_q's word, block w
+        const uint32_t word = sm.rows_w[wl][lane] & rmask;          // row r_q's word, block w
         __syncwarp();
         int64_t ms = 0;
         if (word) {
-          const int64_t* tw = nib + 128 * w;
+          if (p.nib32) {                                            // scaled masses fit int32
+            const int32_t* tw = p.nib32 + 128 * w;
+            int32_t m32 = 0;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+            for (int q = 0; q < 8; ++q) m32 += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+            ms = m32;
+          } else {
+            const int64_t* tw = p.nib + 128 * w;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+          }
         }
         uint32_t* oj = out + (int64_t)j * p.cs;
         if (lane == 31 && g + 1 < p.G) oj[p.brow + (g + 1) * p.G + w] = word;   // row 32(g+1)
@@ -307,6 +311,7 @@ struct ScanParams {
   const uint4* blob;          // M[n] int64, C[n] int64, pred_ptr[n+1], pred_idx[E] (int32)
   int32_t blob_bytes;
   int32_t n, o_pred_ptr, o_pred_idx;
+  int32_t o_nrec, o_drec;     // byte offsets of the node / dependency records in the blob
   const uint32_t* ws;         // chunk workspace from K1 (cs words per candidate)
   int32_t cs, G, brow;
   int64_t n_cand;             // candidates in this chunk
@@ -329,8 +334,10 @@ struct AView {
   uint32_t taddr;
   int tmc;
   int lane;
-  __device__ __forceinline__ uint32_t ld(int k) const {
-    if (TM && k < tmc) {
+  // MODE 0: shared only; 1: decide per access (node < tmc -> TMEM); 2: TMEM only.
+  template <int MODE>
+  __device__ __forceinline__ uint32_t ldm(int k) const {
+    if (TM && (MODE == 2 || (MODE == 1 && k < tmc))) {
       uint32_t v;
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)k) : "memory");
       asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
@@ -338,12 +345,15 @@ struct AView {
     }
     return sm[32 * (k - tmc) + lane];
   }
-  __device__ __forceinline__ void st(int k, uint32_t v) const {
-    if (TM && k < tmc)
+  template <int MODE>
+  __device__ __forceinline__ void stm(int k, uint32_t v) const {
+    if (TM && (MODE == 2 || (MODE == 1 && k < tmc)))
       asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)k), "r"(v) : "memory");
     else
       sm[32 * (k - tmc) + lane] = v;
   }
+  __device__ __forceinline__ uint32_t ld(int k) const { return ldm<TM ? 1 : 0>(k); }
+  __device__ __forceinline__ void st(int k, uint32_t v) const { stm<TM ? 1 : 0>(k, v); }
   __device__ __forceinline__ void st4(int k, uint4 v) const {   // nodes k..k+3, k % 4 == 0
     if (TM && k < tmc)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
@@ -362,32 +372,35 @@ struct AView {
 
 // One node k of the group-g pass for dependency count ND (0..4; ND = 4 also walks any
 // further dependencies).  Specialised so the event loop carries exactly ND free masks.
-template <int ND, typename ET, bool TM>
+// drec[e] = {i, (int32) M_i} (M_i read from the int64 array when ET is int64).
+template <int ND, typename ET, bool TM, int MODE>
 __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk, int e0, int nd,
-                                          const int32_t* __restrict__ pred_idx,
+                                          const int2* __restrict__ drec,
                                           const int64_t* __restrict__ M, const AView<TM>& A, ET* E,
                                           int lane, uint32_t& a_next) {
   uint32_t f[ND > 0 ? ND : 1];
   ET mi[ND > 0 ? ND : 1];
 #pragma unroll
   for (int j = 0; j < ND; ++j) {                                   // FREE_{t,i,k} = R_k & ~A'_i
-    const int i = pred_idx[e0 + j];
+    const int2 d = drec[e0 + j];
+    const int i = d.x;
     const bool nb = (i == k - 1);
-    const uint32_t ai = nb ? a_next : A.ld(i);
+    const uint32_t ai = nb ? a_next : A.template ldm<MODE>(i);
     f[j] = Rk & ~ai;
-    A.st(i, ai | Rk);                                               // A'_i |= R_k
+    A.template stm<MODE>(i, ai | Rk);                               // A'_i |= R_k
     if (nb) a_next = ai | Rk;
-    mi[j] = (ET)M[i];
+    mi[j] = sizeof(ET) == 4 ? (ET)d.y : (ET)M[i];
   }
   if (ND == 4) {
     for (int e = e0 + 4; e < e0 + nd; ++e) {                       // in-degree > 4 (rare)
-      const int i = pred_idx[e];
+      const int2 d = drec[e];
+      const int i = d.x;
       const bool nb = (i == k - 1);
-      const uint32_t ai = nb ? a_next : A.ld(i);
+      const uint32_t ai = nb ? a_next : A.template ldm<MODE>(i);
       uint32_t fx = Rk & ~ai;
-      A.st(i, ai | Rk);
+      A.template stm<MODE>(i, ai | Rk);
       if (nb) a_next = ai | Rk;
-      const ET Mi = (ET)M[i];
+      const ET Mi = sizeof(ET) == 4 ? (ET)d.y : (ET)M[i];
       for (; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
     }
   }
@@ -420,6 +433,51 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
   }
 }
 
+// Walk the quads q = q_hi .. q_lo (nodes 4q+3 .. 4q) of a group pass.  MODE as in AView.
+// nrec[k] = {(int32) M_k, e0, nd, -} with C_k from the int64 array.
+template <typename ET, bool TM, int MODE>
+__device__ __forceinline__ void walk(int q_hi, int q_lo, int nk, int g, bool live, const uint4* sn4,
+                                     const uint32_t* brow, const int4* __restrict__ nrec,
+                                     const int2* __restrict__ drec, const int64_t* __restrict__ M,
+                                     const int64_t* __restrict__ C, const AView<TM>& A, ET* E, int lane,
+                                     uint4& cur, uint32_t& a_next, uint32_t& bword, uint32_t& bnext,
+                                     int64_t& costL) {
+  for (int q = q_hi; q >= q_lo; --q) {
+    const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
+    if ((q & 7) == 7) {                                             // entered a new 32-node block
+      bword = bnext;
+      const int wb = (q >> 3) - 1;
+      bnext = (g > 0 && wb >= 0 && wb < g && live) ? brow[wb] : 0u;
+    }
+#pragma unroll
+    for (int u = 3; u >= 0; --u) {
+      const int k = 4 * q + u;
+      if (k >= nk) continue;                                        // warp-uniform
+      const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
+      const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);   // S_t from S_{t+1} and row 32g
+      A.fence_st();                                                 // earlier stores visible
+      const uint32_t a = a_next;                                    // A'_k = Sn_k | Acc_k (complete)
+      a_next = k > 0 ? A.template ldm<(MODE == 1) ? 1 : MODE>(k - 1) : 0u;   // prefetch
+      const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
+      const uint32_t Rk = (a & ~sw) | diag;                         // a2 seed + a3 closure
+      A.template stm<MODE>(k, Rk);                                  // slot now holds R column
+      if (!__any_sync(FULL, Rk != 0u)) continue;                    // computed in no lane
+      const int4 rec = nrec[k];
+      const ET Mk = sizeof(ET) == 4 ? (ET)rec.x : (ET)M[k];
+      costL += (int64_t)__popc(Rk) * C[k];
+      const int e0 = rec.y, nd = rec.z;
+      switch (nd) {                                                 // warp-uniform
+        case 0: node_step<0, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+        case 1: node_step<1, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+        case 2: node_step<2, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+        case 3: node_step<3, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+        default: node_step<4, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+      }
+    }
+    cur = nxt;
+  }
+}
+
 // ET = int32_t when every M is a multiple of a scale s with sum M/s < 2^30 (the host checks;
 // exact), else int64_t.  M in the blob, the masses and the results are in units of s.
 // TM: A' of nodes < 256 in Tensor Memory (8 warps, one CTA per SM, 512 TMEM columns:
@@ -432,8 +490,9 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
   const int64_t* M = reinterpret_cast<const int64_t*>(smem);
   const int64_t* C = M + n;
   const int32_t* gi = reinterpret_cast<const int32_t*>(smem + 16 * n);
-  const int32_t* pred_ptr = gi + p.o_pred_ptr;
-  const int32_t* pred_idx = gi + p.o_pred_idx;
+  const int4* nrec = reinterpret_cast<const int4*>(smem + p.o_nrec);
+  const int2* drec = reinterpret_cast<const int2*>(smem + p.o_drec);
+  (void)gi;
   unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
   ET* E = reinterpret_cast<ET*>(wr);                               // [32 stages][32 lanes]
   uint32_t* Asm = reinterpret_cast<uint32_t*>(E + 32 * 32);         // [node][lane] (spill part)
@@ -502,39 +561,19 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
     uint32_t bword = (g > 0 && ((nq - 1) >> 3) < g && live) ? brow[(nq - 1) >> 3] : 0u;
     uint32_t bnext = (g > 0 && ((nq - 1) >> 3) >= 1 && ((nq - 1) >> 3) - 1 < g && live)
                          ? brow[((nq - 1) >> 3) - 1] : 0u;
-    for (int q = nq - 1; q >= 0; --q) {
-      const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
-      if ((q & 7) == 7 && q != nq - 1) {                            // entered a new 32-node block
-        bword = bnext;
-        const int wb = (q >> 3) - 1;
-        bnext = (g > 0 && wb >= 0 && wb < g && live) ? brow[wb] : 0u;
-      }
-#pragma unroll
-      for (int u = 3; u >= 0; --u) {
-        const int k = 4 * q + u;
-        if (k >= nk) continue;                                      // warp-uniform
-        const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
-        const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);  // S_t from S_{t+1} and row 32g
-        A.fence_st();                                               // earlier stores visible
-        const uint32_t a = a_next;                                  // A'_k = Sn_k | Acc_k (complete)
-        a_next = k > 0 ? A.ld(k - 1) : 0u;                          // prefetch; fixed up on a push
-        const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
-        const uint32_t Rk = (a & ~sw) | diag;                       // a2 seed + a3 closure
-        A.st(k, Rk);                                                // slot now holds R column
-        if (!__any_sync(FULL, Rk != 0u)) continue;                  // k computed in no lane: no pushes,
-                                                                    // frees or allocations
-        const ET Mk = (ET)M[k];
-        costL += (int64_t)__popc(Rk) * C[k];
-        const int e0 = pred_ptr[k], nd = pred_ptr[k + 1] - e0;
-        switch (nd) {                                               // warp-uniform
-          case 0: node_step<0, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 1: node_step<1, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 2: node_step<2, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          case 3: node_step<3, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-          default: node_step<4, ET, TM>(k, Rk, a, Mk, e0, nd, pred_idx, M, A, E, lane, a_next); break;
-        }
-      }
-      cur = nxt;
+    // the first quad's block word is bword; the walk reloads bword/bnext at block entries
+    // (q & 7 == 7), so prime bnext with the current block for a block-aligned first quad
+    if (((nq - 1) & 7) == 7) bnext = bword;
+    if (!TM) {
+      walk<ET, TM, 0>(nq - 1, 0, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next, bword,
+                      bnext, costL);
+    } else {
+      const int qb = A.tmc >> 2;                                      // quads with k >= tmc: mixed
+      if (nq - 1 >= qb)
+        walk<ET, TM, 1>(nq - 1, qb, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next, bword,
+                        bnext, costL);
+      walk<ET, TM, 2>(min(nq - 1, qb - 1), 0, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next,
+                      bword, bnext, costL);
     }
     // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
     const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
