@@ -164,14 +164,14 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   int occ1 = 0, occ2 = 0;
-  const size_t smem1 = sizeof(cm2::K1Smem);
+  const size_t smem1 = sizeof(cm2::K1Smem) + (g->d_nib32 ? 4 * (size_t)g->nib_entries : 0);
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
       e = cudaFuncSetAttribute(cm2::round_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(cm2::K1Smem));
+                               (int)(sizeof(cm2::K1Smem) + 4 * 128 * 32));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
@@ -269,7 +269,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     rp.s_begin = s0;
     rp.s_count = sc;
     rp.sn = blk;
-    const int64_t warps1 = (int64_t)sc * G;
+    const int64_t warps1 = use_tma ? (int64_t)sc : (int64_t)sc * G;   // TMA K1: a task is one S*
     // one K1 CTA per SM (8 warps, 64 KB, 32k registers): it co-resides with the scan CTA
     // (TMEM variant: 8 warps, ~144 KB, 32k registers), so chunk c+1 streams while c scans.
     const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + 7) / 8, (int64_t)g->sm_count));

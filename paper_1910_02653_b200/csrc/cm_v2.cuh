@@ -136,20 +136,22 @@ struct K1Smem {
 __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char k1smem[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(k1smem);
+  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + sizeof(K1Smem));   // p.nib32 staged (if any)
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
-  const int tasks = p.s_count * p.G;
+  const int G = p.G;
+  if (p.nib32)
+    for (int i = threadIdx.x; i < p.nib_entries; i += blockDim.x) nib32[i] = p.nib32[i];
   if (lane == 0)
     for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wl][st], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
+  __syncthreads();
 
-  // producer cursor: (task, w) sequence of this warp; (ps, pg) decoded once per task
-  int pt = wid, pw = 0, pstage = 0;
-  int ps = pt / p.G, pg = pt - ps * p.G;
+  // A task is one S*: blocks (g, w), g = 0..G-1, w = 0..g.  Producer cursor (ps, pg, pw).
+  int ps = wid, pg = 0, pw = 0, pstage = 0;
   auto issue = [&]() {
-    if (pt >= tasks) return;
+    if (ps >= p.s_count) return;
     if (lane == 0) {
       // the warp's generic reads of this stage (a previous block) precede the async write
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -160,70 +162,68 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
     pstage = pstage + 1 == kStages ? 0 : pstage + 1;
     if (++pw > pg) {
       pw = 0;
-      pt += nw;
-      ps = pt / p.G;
-      pg = pt - ps * p.G;
+      if (++pg == G) { pg = 0; ps += nw; }
     }
   };
   for (int d = 0; d < kStages - 1; ++d) issue();
 
   int cstage = 0;
   uint32_t phase_bits = 0u;                                         // bit st = parity of stage st
-  for (int task = wid; task < tasks; task += nw) {
-    const int s = task / p.G;
-    const int g = task - s * p.G;
+  for (int s = wid; s < p.s_count; s += nw) {
     uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
-    const int rq = 32 * g + lane + 1;                               // row owned by this lane
-    int64_t mass[4] = {0, 0, 0, 0};
-    for (int w = 0; w <= g; ++w) {
-      issue();                                                      // keep kStages-1 blocks ahead
-      mbar_wait(&sm.bar[wl][cstage], (phase_bits >> cstage) & 1u);
-      phase_bits ^= 1u << cstage;
-      const float(*tl)[32] = sm.tile[wl][cstage];
-      float x[32];
+    for (int g = 0; g < G; ++g) {
+      const int rq = 32 * g + lane + 1;                             // row owned by this lane
+      int64_t mass[4] = {0, 0, 0, 0};
+      for (int w = 0; w <= g; ++w) {
+        issue();                                                    // keep kStages-1 blocks ahead
+        mbar_wait(&sm.bar[wl][cstage], (phase_bits >> cstage) & 1u);
+        phase_bits ^= 1u << cstage;
+        const float(*tl)[32] = sm.tile[wl][cstage];
+        float x[32];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
-      __syncwarp();                                                 // all lanes read the tile
-      cstage = cstage + 1 == kStages ? 0 : cstage + 1;
-      // Row-word mask of this lane's row: nodes i < rq of block w (strict lower triangle) and
-      // rq < n.  Masking the row words masks the transposed columns too; zero-filled or
-      // upper-triangle tile entries never leak.
-      const int cnt = rq < p.n ? min(max(rq - 32 * w, 0), 32) : 0;
-      const uint32_t rmask = cnt >= 32 ? FULL : ((1u << cnt) - 1u);
-      const int node = 32 * w + lane;
+        for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
+        __syncwarp();                                               // all lanes read the tile
+        cstage = cstage + 1 == kStages ? 0 : cstage + 1;
+        // Row-word mask of this lane's row: nodes i < rq of block w (strict lower triangle)
+        // and rq < n.  Masking the row words masks the transposed columns too; zero-filled
+        // or upper-triangle tile entries never leak.
+        const int cnt = rq < p.n ? min(max(rq - 32 * w, 0), 32) : 0;
+        const uint32_t rmask = cnt >= 32 ? FULL : ((1u << cnt) - 1u);
+        const int node = 32 * w + lane;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j >= p.nt) break;
-        const float th = __ldg(p.theta + p.th0 + j);
+        for (int j = 0; j < 4; ++j) {
+          if (j >= p.nt) break;
+          const float th = __ldg(p.theta + p.th0 + j);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) sm.rows_w[wl][q] = __ballot_sync(FULL, x[q] > th);
-        __syncwarp();
-        const uint32_t word = sm.rows_w[wl][lane] & rmask;          // row r_q's word, block w
-        __syncwarp();
-        int64_t ms = 0;
-        if (word) {
-          if (p.nib32) {                                            // scaled masses fit int32
-            const int32_t* tw = p.nib32 + 128 * w;
-            int32_t m32 = 0;
+          for (int q = 0; q < 32; ++q) sm.rows_w[wl][q] = __ballot_sync(FULL, x[q] > th);
+          __syncwarp();
+          const uint32_t word = sm.rows_w[wl][lane] & rmask;        // row r_q's word, block w
+          __syncwarp();
+          int64_t ms = 0;
+          if (word) {
+            if (p.nib32) {                                          // scaled masses fit int32
+              const int32_t* tw = nib32 + 128 * w;
+              int32_t m32 = 0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) m32 += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
-            ms = m32;
-          } else {
-            const int64_t* tw = p.nib + 128 * w;
+              for (int q = 0; q < 8; ++q) m32 += tw[16 * q + ((word >> (4 * q)) & 15u)];
+              ms = m32;
+            } else {
+              const int64_t* tw = p.nib + 128 * w;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+              for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
+            }
           }
+          uint32_t* oj = out + (int64_t)j * p.cs;
+          if (lane == 31 && g + 1 < G) oj[p.brow + (g + 1) * G + w] = word;   // row 32(g+1)
+          oj[grp_off(g) + node] = transpose32(word, lane);
+          mass[j] += ms;
         }
-        uint32_t* oj = out + (int64_t)j * p.cs;
-        if (lane == 31 && g + 1 < p.G) oj[p.brow + (g + 1) * p.G + w] = word;   // row 32(g+1)
-        oj[grp_off(g) + node] = transpose32(word, lane);
-        mass[j] += ms;
       }
-    }
-    if (rq < p.n) {
+      if (rq < p.n) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+        for (int j = 0; j < 4; ++j)
+          if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+      }
     }
   }
 }
