@@ -164,20 +164,27 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   int occ1 = 0, occ2 = 0;
-  const size_t smem1 = sizeof(cm2::K1Smem) + (g->d_nib32 ? 4 * (size_t)g->nib_entries : 0);
+  const int nt_max = std::min(4, a->n_theta);
+  const size_t smem1 = cm2::k1_smem_bytes(nt_max, g->d_nib32 ? g->nib_entries : 0);
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
-      e = cudaFuncSetAttribute(cm2::round_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(sizeof(cm2::K1Smem) + 4 * 128 * 32));
-      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::round_tma_kernel<1>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4>)}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cm2::k1_smem_bytes(4, 128 * 32));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return cuda_fail(e, "carveout(round_tma_kernel)");
+      }
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel),
                              reinterpret_cast<const void*>(cm2::round_ldg_kernel)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
@@ -197,11 +204,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const cuuint32_t box[3] = {32, 32, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
-  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel, 256, smem1);
+  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel<4>, 256, smem1);
   else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_ldg_kernel, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
@@ -277,8 +284,14 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
       rp.th0 = th0;
       rp.nt = std::min(4, a->n_theta - th0);
-      if (use_tma) cm2::round_tma_kernel<<<grid1, 256, smem1, g->st_round>>>(rp, tmap);
-      else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
+      if (use_tma) {
+        switch (rp.nt) {
+          case 1: cm2::round_tma_kernel<1><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
+          case 2: cm2::round_tma_kernel<2><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
+          case 3: cm2::round_tma_kernel<3><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
+          default: cm2::round_tma_kernel<4><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
+        }
+      } else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
     }
     if (tr) cudaEventRecord(trace_event(4 * c + 1), g->st_round);
     e = cudaEventRecord(g->ev_round[b], g->st_round);

@@ -73,6 +73,34 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
+// The same transpose with the per-lane select folded into a rotate: t = rotl(y, s_j) with
+// s_j = j (lane bit j clear) or 32 - j (set); the bits a rotate wraps around land exactly
+// where the stage's keep-mask K_j drops them.  3 instructions per stage (SHFL, SHF.L.W, LOP3).
+struct Transposer {
+  uint32_t K[5];
+  uint32_t sh[5];
+  __device__ __forceinline__ explicit Transposer(int lane) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int j = 16 >> k;
+      const uint32_t M = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                       : j == 2 ? 0x33333333u : 0x55555555u;
+      const bool hi = (lane & j) != 0;
+      K[k] = hi ? ~M : M;
+      sh[k] = hi ? 32u - j : (uint32_t)j;
+    }
+  }
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t y = __shfl_xor_sync(FULL, x, 16 >> k);
+      const uint32_t t = __funnelshift_l(y, y, sh[k]);
+      x = (x & K[k]) | (t & ~K[k]);
+    }
+    return x;
+  }
+};
+
 // ------------------------------------------------------------------------------------ K1
 struct RoundParams {
   const float* sstar;
@@ -117,27 +145,41 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, 
       :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
 }
 
-// K1 for the dense layout.  Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31
-// (the S_{t+1} rows of the group's stages), 32 nodes (block w) at a time.  One elected lane
-// loads block w with a single 3-D tensor-map TMA (rows >= n are zero-filled) into a
-// 3-stage shared ring (one mbarrier per stage), two blocks ahead of the consumer.  Consumption: lane = node, one LDS + one
-// compare (a1, strict fp32 '>', NaN -> 0) + one ballot per row, which is the packed row
-// word.  The row words go through a 32-word shared slot to lane q, which transposes them
-// into column words and adds its row's checkpoint mass mass_r = sum_{i in S_r} M_i (the
-// Eq. 6 sum) from 4-bit tables.
+// K1 for the dense layout.  Per S* the warp walks the blocks (g, w), g = 0..G-1, w = 0..g:
+// rows r = 32g+1+l, l = 0..31 (the S_{t+1} rows of group g's stages) x nodes 32w..32w+31.
+// One elected lane loads a block with a single 3-D tensor-map TMA (rows >= n zero-filled) in
+// the 128-byte swizzle (16-byte chunk c of tile row l lands at chunk c ^ (l & 7)), so lane l
+// reads its own row with 8 conflict-free LDS.128.  One ballot per node q of x[q] > theta
+// (Alg. 2 line 1) yields node q's column word over the 32 rows -- the form K2
+// consumes; the 32 words pass through a 32-word shared slot to lane q, which masks them to
+// the strict lower triangle, stores them, and transposes them into row words for the row's
+// checkpoint mass mass_r = sum_{i in S_r} M_i (the Eq. 6 sum, from 4-bit
+// tables) and for row 32(g+1)'s word (the brow operand of K2).
 constexpr int kStages = 2;     // 64 KB per CTA: co-resides with the TMEM scan CTA (144 KB)
 constexpr int kK1Warps = 8;
+// Shared layout (bytes from a 1024-aligned base): tiles, mbarriers, NT column-word slots per
+// warp (one per threshold, so the NT chains interleave), then the staged int32 mass tables.
 struct K1Smem {
-  float tile[kK1Warps][kStages][32][32];
+  float tile[kK1Warps][kStages][32][32];      // 4 KB tiles, 1024-byte aligned (swizzle atom)
   uint64_t bar[kK1Warps][kStages];
-  uint32_t rows_w[kK1Warps][32];
 };
+__host__ __device__ constexpr size_t k1_cols_off() { return sizeof(K1Smem); }
+__host__ __device__ constexpr size_t k1_nib_off(int nt) { return sizeof(K1Smem) + (size_t)kK1Warps * nt * 128; }
+// dynamic bytes to request: + 1024 slack for aligning the base
+__host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries) {
+  return k1_nib_off(nt) + 4 * (size_t)nib_entries + 1024;
+}
 
-__global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ __align__(128) unsigned char k1smem[];
+// NT = thresholds per pass (1..4, a compile-time count so the per-threshold work of one block
+// -- ballots, mass lookups, transposes -- forms NT independent instruction chains).
+template <int NT>
+__global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char k1raw[];
+  unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
   K1Smem& sm = *reinterpret_cast<K1Smem*>(k1smem);
-  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + sizeof(K1Smem));   // p.nib32 staged (if any)
+  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT));   // p.nib32 staged (if any)
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint32_t(*cols_w)[32] = reinterpret_cast<uint32_t(*)[32]>(k1smem + k1_cols_off()) + NT * wl;
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
   const int G = p.G;
@@ -147,14 +189,21 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
     for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wl][st], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  float th[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) th[j] = p.theta[p.th0 + j];
+  const Transposer transpose(lane);
+  const bool scaled32 = p.nib32 != nullptr;
+  const uint32_t row_base = smem_u32(&sm.tile[wl][0][lane][0]);     // stage 0, this lane's row
+  const uint32_t swz = (uint32_t)(lane & 7) << 4;
 
-  // A task is one S*: blocks (g, w), g = 0..G-1, w = 0..g.  Producer cursor (ps, pg, pw).
+  // Producer cursor (ps, pg, pw) runs kStages-1 blocks ahead of the consumer.  No proxy
+  // fence before re-filling a stage: its previous contents were consumed (ballots issued on
+  // the loaded values, then __syncwarp) before the refill is issued.
   int ps = wid, pg = 0, pw = 0, pstage = 0;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
     if (lane == 0) {
-      // the warp's generic reads of this stage (a previous block) precede the async write
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
       tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
                   &sm.bar[wl][pstage]);
@@ -173,56 +222,74 @@ __global__ void __launch_bounds__(256) round_tma_kernel(const RoundParams p, con
     uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
     for (int g = 0; g < G; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
-      int64_t mass[4] = {0, 0, 0, 0};
+      // rows of the group that exist (r < n): bits [0, hi)
+      const int hi = p.n - 1 - 32 * g;
+      const uint32_t rows_ok = hi >= 32 ? FULL : (hi <= 0 ? 0u : (1u << hi) - 1u);
+      int64_t mass[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) mass[j] = 0;
       for (int w = 0; w <= g; ++w) {
-        issue();                                                    // keep kStages-1 blocks ahead
+        issue();
         mbar_wait(&sm.bar[wl][cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
-        const float(*tl)[32] = sm.tile[wl][cstage];
+        const uint32_t rb = row_base + (uint32_t)cstage * (32u * 32u * 4u);
         float x[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) x[q] = tl[q][lane];
-        __syncwarp();                                               // all lanes read the tile
+        for (int c = 0; c < 8; ++c) {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + (((uint32_t)c << 4) ^ swz)));
+          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        }
         cstage = cstage + 1 == kStages ? 0 : cstage + 1;
-        // Row-word mask of this lane's row: nodes i < rq of block w (strict lower triangle)
-        // and rq < n.  Masking the row words masks the transposed columns too; zero-filled
-        // or upper-triangle tile entries never leak.
-        const int cnt = rq < p.n ? min(max(rq - 32 * w, 0), 32) : 0;
-        const uint32_t rmask = cnt >= 32 ? FULL : ((1u << cnt) - 1u);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int q = 0; q < 32; ++q) cols_w[j][q] = __ballot_sync(FULL, x[q] > th[j]);
+        __syncwarp();                                               // tile read, ballots stored
+        // Column mask of node i = 32w + lane: rows r = 32g+1+b with i < r (strict lower
+        // triangle: b >= 32(w-g) + lane) and r < n.  Zero-filled / upper entries never leak.
+        const int lo = 32 * (w - g) + lane;
+        const uint32_t cmask = rows_ok & (lo <= 0 ? FULL : (lo >= 32 ? 0u : FULL << lo));
+        uint32_t word[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) word[j] = cols_w[j][lane] & cmask;   // node i's column
+        __syncwarp();
         const int node = 32 * w + lane;
+        const int brow_at = p.brow + (g + 1) * G + w;               // row 32(g+1)'s word (lane 31)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j >= p.nt) break;
-          const float th = __ldg(p.theta + p.th0 + j);
-#pragma unroll
-          for (int q = 0; q < 32; ++q) sm.rows_w[wl][q] = __ballot_sync(FULL, x[q] > th);
-          __syncwarp();
-          const uint32_t word = sm.rows_w[wl][lane] & rmask;        // row r_q's word, block w
-          __syncwarp();
-          int64_t ms = 0;
-          if (word) {
-            if (p.nib32) {                                          // scaled masses fit int32
-              const int32_t* tw = nib32 + 128 * w;
-              int32_t m32 = 0;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) m32 += tw[16 * q + ((word >> (4 * q)) & 15u)];
-              ms = m32;
-            } else {
-              const int64_t* tw = p.nib + 128 * w;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
-            }
-          }
+        for (int j = 0; j < NT; ++j) {
           uint32_t* oj = out + (int64_t)j * p.cs;
-          if (lane == 31 && g + 1 < G) oj[p.brow + (g + 1) * G + w] = word;   // row 32(g+1)
-          oj[grp_off(g) + node] = transpose32(word, lane);
-          mass[j] += ms;
+          oj[grp_off(g) + node] = word[j];
+          word[j] = transpose(word[j]);                             // row rq's word over block w
+          if (lane == 31 && g + 1 < G) oj[brow_at] = word[j];
+        }
+        if (scaled32) {                                             // scaled masses fit int32
+          const unsigned char* tb = reinterpret_cast<const unsigned char*>(nib32 + 128 * w);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            int32_t m32 = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t off = q == 0 ? (word[j] << 2) & 0x3Cu : (word[j] >> (4 * q - 2)) & 0x3Cu;
+              m32 += *reinterpret_cast<const int32_t*>(tb + 64 * q + off);
+            }
+            mass[j] += m32;
+          }
+        } else {
+          const int64_t* tw = p.nib + 128 * w;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            int64_t ms = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word[j] >> (4 * q)) & 15u));
+            mass[j] += ms;
+          }
         }
       }
       if (rq < p.n) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+        for (int j = 0; j < NT; ++j) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
       }
     }
   }
