@@ -66,7 +66,7 @@ int cpw_override() {
   const char* e = std::getenv("CM_CPW");
   return e ? std::atoi(e) : 0;
 }
-constexpr int64_t kDefaultWsBytes = int64_t(256) << 20;  // two 128 MB chunk buffers: >= 3 waves of scan tasks
+constexpr int64_t kDefaultWsBytes = int64_t(512) << 20;  // two 256 MB chunk buffers: ~6 waves of scan tasks per chunk
 }  // namespace
 
 
@@ -533,7 +533,9 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
   }
   if (e == cudaSuccess) {
     const int64_t per = cand_bytes(n);
-    g->ws_bytes = std::max<int64_t>(per * 1024, (kDefaultWsBytes / (64 * per)) * 64 * per);
+    int64_t want = kDefaultWsBytes;
+    if (const char* env = std::getenv("CM_WS_MB")) want = std::max<int64_t>(1, std::atoll(env)) << 20;   // tuning
+    g->ws_bytes = std::max<int64_t>(per * 1024, (want / (64 * per)) * 64 * per);
     e = cudaMalloc(&g->d_ws, g->ws_bytes);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->st_round, cudaStreamNonBlocking);
