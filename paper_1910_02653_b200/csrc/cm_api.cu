@@ -40,9 +40,10 @@ struct cm_graph {
   void* d_blob = nullptr;
   // v2 (stage-sliced) path
   int32_t blob2_bytes = 0;            // M/mscale, C, pred_ptr, pred_idx, node/dep records
-  int32_t o_nrec = 0, o_drec = 0;
+  int32_t o_nrec = 0, o_drec = 0, o_qinfo = 0;
   int64_t mscale = 1;                 // gcd of all M (>= 1); the scan works in units of it
   bool scan32 = false;                // sum M / mscale < 2^30: int32 per-stage state
+  int32_t n_slot = 0;                 // nodes with a non-adjacent user (K2 A' slots)
   void* d_blob2 = nullptr;
   void* d_nib = nullptr;              // K1 nibble tables of M (checkpoint mass, Eq. 6)
   void* d_nib32 = nullptr;            // int32 copy when scan32 (every row mass < 2^30)
@@ -91,8 +92,8 @@ EncodeTiledFn encode_tiled() {
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
-size_t scan_warp_bytes(int n, bool s32, bool tm) {
-  const int spill = std::max(0, ((n + 3) & ~3) - (tm ? 256 : 0));   // A' nodes kept in shared memory
+size_t scan_warp_bytes(int n_slot, bool s32, bool tm) {
+  const int spill = std::max(0, n_slot - (tm ? 256 : 0));          // A' slots kept in shared memory
   return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * spill;
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
@@ -121,6 +122,12 @@ bool tmem_enabled() {
   return !(e && std::strcmp(e, "0") == 0);
 }
 
+// tuning switches: CM_EVICT_FIRST=1 (default off), CM_PREFETCH=0 (default on)
+int env_flag(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
   const int G = (n + 31) / 32;
@@ -137,8 +144,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   // Scan kernel variant: A' in Tensor Memory (+ shared spill) with 8 warps per SM when that
   // fits, else all in shared memory with as many warps as fit.
   const size_t fixed = (size_t)g->blob2_bytes;
-  const bool tm = tmem_enabled() && fixed + 8 * scan_warp_bytes(n, g->scan32, true) + 1024 <= (size_t)g->smem_optin;
-  const size_t wb = scan_warp_bytes(n, g->scan32, tm);
+  const bool tm = tmem_enabled() && fixed + 8 * scan_warp_bytes(g->n_slot, g->scan32, true) + 1024 <= (size_t)g->smem_optin;
+  const size_t wb = scan_warp_bytes(g->n_slot, g->scan32, tm);
   if (fixed + wb > (size_t)g->smem_optin) return fail(CM_ERANGE, "scan kernel: shared memory exceeded");
   const int wpc = tm ? 8 : (int)std::min<size_t>(8, ((size_t)g->smem_optin - fixed) / wb);
   const size_t smem2 = fixed + wb * wpc;
@@ -229,6 +236,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   rp.nib32 = reinterpret_cast<const int32_t*>(g->d_nib32);
   rp.nib_entries = g->nib_entries;
   rp.brow = cm2::brow_off(n);
+  rp.evict_first = env_flag("CM_EVICT_FIRST", 0);   // measured: -2%
 
   cm2::ScanParams sp;
   sp.blob = reinterpret_cast<const uint4*>(g->d_blob2);
@@ -238,6 +246,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   sp.o_pred_idx = n + 1;
   sp.o_nrec = g->o_nrec;
   sp.o_drec = g->o_drec;
+  sp.n_slot = g->n_slot;
+  sp.o_qinfo = g->o_qinfo;
+  sp.prefetch = env_flag("CM_PREFETCH", 1);
   sp.cs = cs;
   sp.G = G;
   sp.brow = cm2::brow_off(n);
@@ -489,11 +500,19 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     g->scan32 = tot < (int64_t(1) << 30);
     if (!g->scan32) g->mscale = 1;
   }
-  // + node records {(int32) M_k, e0, nd, 0} and dependency records {i, (int32) M_i}
+  // + node records {(int32) M_k, e0, ndf | adj << 16, slot_k or -1} and far-dependency
+  // records {slot_i | i << 16, (int32) M_i}.  adj: k-1 is a dependency of k (its A' term
+  // rides in a register); slot: k has a user other than k+1, so its A' needs storage.
+  std::vector<int32_t> slot(n, -1);
+  for (int i = 0; i < n; ++i)
+    for (int32_t j : users[i])
+      if (j != i + 1) { slot[i] = g->n_slot++; break; }
   size_t base2 = (16 * (size_t)n + 4 * (size_t)(n + 1 + E) + 15) & ~size_t(15);
   g->o_nrec = (int32_t)base2;
   g->o_drec = (int32_t)(base2 + 16 * (size_t)n);
-  size_t bytes2 = (base2 + 16 * (size_t)n + 8 * (size_t)E + 15) & ~size_t(15);
+  g->o_qinfo = (int32_t)(base2 + 16 * (size_t)n + 8 * (size_t)E);
+  const int nquad = (n + 3) / 4;
+  size_t bytes2 = (base2 + 16 * (size_t)n + 8 * (size_t)E + 4 * (size_t)nquad + 15) & ~size_t(15);
   g->blob2_bytes = (int32_t)bytes2;
   std::vector<unsigned char> blob2(bytes2, 0);
   std::memcpy(blob2.data(), blob.data(), 16 * (size_t)n + 4 * (size_t)(n + 1 + E));
@@ -501,15 +520,31 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
   {
     int32_t* nr = reinterpret_cast<int32_t*>(blob2.data() + g->o_nrec);
     int32_t* dr = reinterpret_cast<int32_t*>(blob2.data() + g->o_drec);
+    int32_t ef = 0;
     for (int k = 0; k < n; ++k) {
+      int32_t ndf = 0, adj = 0;
       nr[4 * k + 0] = (int32_t)(mem[k] / g->mscale);      // meaningful when scan32
-      nr[4 * k + 1] = pred_ptr[k];
-      nr[4 * k + 2] = pred_ptr[k + 1] - pred_ptr[k];
-      nr[4 * k + 3] = 0;
+      nr[4 * k + 1] = ef;
       for (int e = pred_ptr[k]; e < pred_ptr[k + 1]; ++e) {
-        dr[2 * e + 0] = pidx[e];
-        dr[2 * e + 1] = (int32_t)(mem[pidx[e]] / g->mscale);
+        const int32_t i = pidx[e];
+        if (i == k - 1) { adj = 1; continue; }
+        dr[2 * ef + 0] = slot[i] | (i << 16);
+        dr[2 * ef + 1] = (int32_t)(mem[i] / g->mscale);
+        ++ef;
+        ++ndf;
       }
+      nr[4 * k + 2] = ndf | (adj << 16);
+      nr[4 * k + 3] = slot[k];
+    }
+    int32_t* qi = reinterpret_cast<int32_t*>(blob2.data() + g->o_qinfo);
+    for (int q = 0; q < nquad; ++q) {
+      int32_t first = -1, msk = 0;
+      for (int j = 0; j < 4 && 4 * q + j < n; ++j)
+        if (slot[4 * q + j] >= 0) {
+          if (first < 0) first = slot[4 * q + j];
+          msk |= 1 << j;
+        }
+      qi[q] = (first < 0 ? 0 : first) | (msk << 16);
     }
   }
   e = cudaMalloc(&g->d_blob2, bytes2);
@@ -626,7 +661,7 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
   if (n_cand == 0) return CM_OK;
-  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(n, g->scan32, false) <= (size_t)g->smem_optin) {
+  if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(g->n_slot, g->scan32, false) <= (size_t)g->smem_optin) {
     cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);

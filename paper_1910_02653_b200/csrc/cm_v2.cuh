@@ -119,6 +119,7 @@ struct RoundParams {
   const int32_t* nib32;       // the same in int32 when every row mass fits (else nullptr)
   int32_t nib_entries;        // 128 * G
   int32_t brow;               // word offset of brow in a candidate block
+  int32_t evict_first;        // S* loads with an L2 evict-first policy
 };
 
 // ---- bulk-async copy + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS) ----
@@ -139,10 +140,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "@!p bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 // 3-D tensor-map TMA: box {32 nodes, 32 rows, 1 S*} at (x = node, y = row, z = S*).
+// S* is read exactly once: the loads carry an L2 evict-first policy so the stream does not
+// push the K1 -> K2 workspace out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
       :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(ptr));
 }
 
 // K1 for the dense layout.  Per S* the warp walks the blocks (g, w), g = 0..G-1, w = 0..g:
@@ -195,6 +213,7 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t row_base = smem_u32(&sm.tile[wl][0][lane][0]);     // stage 0, this lane's row
+  const uint64_t pol = p.evict_first ? l2_evict_first_policy() : 0ull;
   const uint32_t swz = (uint32_t)(lane & 7) << 4;
 
   // Producer cursor (ps, pg, pw) runs kStages-1 blocks ahead of the consumer.  No proxy
@@ -205,8 +224,12 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
     if (ps >= p.s_count) return;
     if (lane == 0) {
       mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
-      tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
-                  &sm.bar[wl][pstage]);
+      if (pol)
+        tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
+                    &sm.bar[wl][pstage], pol);
+      else
+        tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
+                    &sm.bar[wl][pstage]);
     }
     pstage = pstage + 1 == kStages ? 0 : pstage + 1;
     if (++pw > pg) {
@@ -372,14 +395,21 @@ __global__ void __launch_bounds__(256) round_ldg_kernel(const RoundParams p) {
 // c0 + l.  The stages of different groups never interact (stage t needs only S_t, S_{t+1}
 // and the graph), so a group pass is a complete, independent evaluation of its 32 stages;
 // all lanes walk the same node range k = min(n,32g+32)-1 .. 0 in lockstep.
-// Shared memory per warp: Sn[node][lane], Acc[node][lane] (u32) and E[stage][lane] (int64),
-// every access lane-contiguous (bank-conflict free).
+//
+// A'_i = Sn_i | Acc_i is kept only where it has to be: a node whose only user is i+1 (the
+// "adjacent" edge i -> i+1) needs no storage -- its Acc is one register carried from step
+// i+1 to step i.  Nodes with a non-adjacent user get a slot (host-assigned, nrec.w), slots
+// < 256 in Tensor Memory, the rest in shared memory.  Per warp in shared memory: E[stage][lane]
+// and the spilled slots [slot][lane].
 struct ScanParams {
-  const uint4* blob;          // M[n] int64, C[n] int64, pred_ptr[n+1], pred_idx[E] (int32)
+  const uint4* blob;          // M[n] int64, C[n] int64, pred_ptr, pred_idx, nrec, drec
   int32_t blob_bytes;
   int32_t n, o_pred_ptr, o_pred_idx;
   int32_t o_nrec, o_drec;     // byte offsets of the node / dependency records in the blob
-  const uint32_t* ws;         // chunk workspace from K1 (cs words per candidate)
+  int32_t n_slot;             // nodes with a non-adjacent user
+  int32_t o_qinfo;            // byte offset of the per-quad slot info (first slot | mask << 16)
+  int32_t prefetch;           // L2-prefetch the warp's next task
+  uint32_t* ws;               // chunk workspace from K1 (cs words per candidate)
   int32_t cs, G, brow;
   int64_t n_cand;             // candidates in this chunk
   int32_t n_batch;            // ceil(n_cand / 32)
@@ -390,90 +420,51 @@ struct ScanParams {
   int32_t warp_bytes;         // shared bytes per warp region
 };
 
-// A' storage of one warp.  TM = false: shared memory [node][lane].  TM = true: nodes < tmc
-// live in Tensor Memory -- lane = TMEM lane (this warp's 32-lane quarter), node = TMEM
+// Slot storage of one warp.  TM = false: shared memory [slot][lane].  TM = true: slots < tmc
+// live in Tensor Memory -- lane = TMEM lane (this warp's 32-lane quarter), slot = TMEM
 // column, accessed with tcgen05.ld/st.32x32b (one column, all 32 lanes, uniform address)
-// -- and nodes >= tmc spill to shared memory.  Stores are made visible to later loads by
-// tcgen05.wait::st, issued once per node step (fence_st).
+// -- and slots >= tmc spill to shared memory.  A load after a store of the same column is
+// ordered by tcgen05.wait::st (the walk tracks pending stores).
 template <bool TM>
 struct AView {
   uint32_t* sm;
   uint32_t taddr;
   int tmc;
   int lane;
-  // MODE 0: shared only; 1: decide per access (node < tmc -> TMEM); 2: TMEM only.
+  // MODE 0: shared only; 1: decide per access (slot < tmc -> TMEM); 2: TMEM only.
   template <int MODE>
-  __device__ __forceinline__ uint32_t ldm(int k) const {
-    if (TM && (MODE == 2 || (MODE == 1 && k < tmc))) {
-      uint32_t v;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)k) : "memory");
-      asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
-      return v;
-    }
-    return sm[32 * (k - tmc) + lane];
-  }
+  __device__ __forceinline__ bool in_tmem(int s) const { return TM && (MODE == 2 || (MODE == 1 && s < tmc)); }
   template <int MODE>
-  __device__ __forceinline__ void stm(int k, uint32_t v) const {
-    if (TM && (MODE == 2 || (MODE == 1 && k < tmc)))
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)k), "r"(v) : "memory");
+  __device__ __forceinline__ uint32_t ld_async(int s) const {   // TMEM: value valid after wait_ld()
+    uint32_t v;
+    if (in_tmem<MODE>(s))
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)s) : "memory");
     else
-      sm[32 * (k - tmc) + lane] = v;
+      v = sm[32 * (s - tmc) + lane];
+    return v;
   }
-  __device__ __forceinline__ uint32_t ld(int k) const { return ldm<TM ? 1 : 0>(k); }
-  __device__ __forceinline__ void st(int k, uint32_t v) const { stm<TM ? 1 : 0>(k, v); }
-  __device__ __forceinline__ void st4(int k, uint4 v) const {   // nodes k..k+3, k % 4 == 0
-    if (TM && k < tmc)
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
-                   :: "r"(taddr + (uint32_t)k), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-    else {
-      sm[32 * (k + 0 - tmc) + lane] = v.x;
-      sm[32 * (k + 1 - tmc) + lane] = v.y;
-      sm[32 * (k + 2 - tmc) + lane] = v.z;
-      sm[32 * (k + 3 - tmc) + lane] = v.w;
-    }
+  __device__ __forceinline__ void wait_ld(uint32_t& v) const {
+    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
   }
-  __device__ __forceinline__ void fence_st() const {
+  template <int MODE>
+  __device__ __forceinline__ void st(int s, uint32_t v) const {
+    if (in_tmem<MODE>(s))
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)s), "r"(v) : "memory");
+    else
+      sm[32 * (s - tmc) + lane] = v;
+  }
+  __device__ __forceinline__ void wait_st() const {
     if (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
 };
 
-// One node k of the group-g pass for dependency count ND (0..4; ND = 4 also walks any
-// further dependencies).  Specialised so the event loop carries exactly ND free masks.
-// drec[e] = {i, (int32) M_i} (M_i read from the int64 array when ET is int64).
-template <int ND, typename ET, bool TM, int MODE>
-__device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk, int e0, int nd,
-                                          const int2* __restrict__ drec,
-                                          const int64_t* __restrict__ M, const AView<TM>& A, ET* E,
-                                          int lane, uint32_t& a_next) {
-  uint32_t f[ND > 0 ? ND : 1];
-  ET mi[ND > 0 ? ND : 1];
-#pragma unroll
-  for (int j = 0; j < ND; ++j) {                                   // FREE_{t,i,k} = R_k & ~A'_i
-    const int2 d = drec[e0 + j];
-    const int i = d.x;
-    const bool nb = (i == k - 1);
-    const uint32_t ai = nb ? a_next : A.template ldm<MODE>(i);
-    f[j] = Rk & ~ai;
-    A.template stm<MODE>(i, ai | Rk);                               // A'_i |= R_k
-    if (nb) a_next = ai | Rk;
-    mi[j] = sizeof(ET) == 4 ? (ET)d.y : (ET)M[i];
-  }
-  if (ND == 4) {
-    for (int e = e0 + 4; e < e0 + nd; ++e) {                       // in-degree > 4 (rare)
-      const int2 d = drec[e];
-      const int i = d.x;
-      const bool nb = (i == k - 1);
-      const uint32_t ai = nb ? a_next : A.template ldm<MODE>(i);
-      uint32_t fx = Rk & ~ai;
-      A.template stm<MODE>(i, ai | Rk);
-      if (nb) a_next = ai | Rk;
-      const ET Mi = sizeof(ET) == 4 ? (ET)d.y : (ET)M[i];
-      for (; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
-    }
-  }
-  const uint32_t selff = Rk & ~a;                                   // FREE_{t,k,k}
-  // every free at k lies in a stage that computes k: E = max(E - GC(k), 0) + M_k.
-  // Up to four stage bits per round: their loads issue together (latency, not issue, bound).
+// Events of one computing node k: for every stage bit b of R_k (stage b computes k), in the
+// backward walk, first the frees at k (Eq. 9: the masks f_j with masses m_j, and the i = k
+// self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k.  NM dependency
+// masks (compile-time), up to four stage bits per round (their loads issue together).
+template <int NM, typename ET>
+__device__ __forceinline__ void events(uint32_t Rk, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
+                                       ET* E, int lane) {
   for (uint32_t x = Rk; x;) {
     int b[4];
     bool v[4];
@@ -488,10 +479,10 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
     for (int u = 0; u < 4; ++u) ev[u] = v[u] ? E[32 * b[u] + lane] : (ET)0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if ((selff >> b[u]) & 1u) ev[u] -= Mk;
+      if ((sf >> b[u]) & 1u) ev[u] -= Mk;
 #pragma unroll
-      for (int j = 0; j < ND; ++j)
-        if ((f[j] >> b[u]) & 1u) ev[u] -= mi[j];
+      for (int j = 0; j < NM; ++j)
+        if ((f[j] >> b[u]) & 1u) ev[u] -= m[j];
       ev[u] = (ev[u] > 0 ? ev[u] : (ET)0) + Mk;
     }
 #pragma unroll
@@ -500,16 +491,77 @@ __device__ __forceinline__ void node_step(int k, uint32_t Rk, uint32_t a, ET Mk,
   }
 }
 
-// Walk the quads q = q_hi .. q_lo (nodes 4q+3 .. 4q) of a group pass.  MODE as in AView.
-// nrec[k] = {(int32) M_k, e0, nd, -} with C_k from the int64 array.
-template <typename ET, bool TM, int MODE>
-__device__ __forceinline__ void walk(int q_hi, int q_lo, int nk, int g, bool live, const uint4* sn4,
+// The far (non-adjacent) dependencies of node k (NDF of them; NDF = 3 also walks any further
+// ones, applying their frees first), the adjacent one (mask fa, mass ma; zero when absent),
+// then the events.  drec[e] = {slot_i | i << 16, (int32) M_i}.
+template <int NDF, typename ET, bool TM, int MODE>
+__device__ __forceinline__ void node_step(uint32_t Rk, uint32_t sf, ET Mk, uint32_t fa, ET ma, int e0, int ndf,
+                                          const int2* __restrict__ drec, const int64_t* __restrict__ M,
+                                          const AView<TM>& A, ET* E, int lane, bool& st_pending) {
+  uint32_t f[NDF + 1];
+  ET m[NDF + 1];
+  f[NDF] = fa;
+  m[NDF] = ma;
+  if (NDF > 0) {
+    int sl[NDF > 0 ? NDF : 1];
+    uint32_t ai[NDF > 0 ? NDF : 1];
+#pragma unroll
+    for (int j = 0; j < NDF; ++j) {
+      const int2 d = drec[e0 + j];
+      sl[j] = d.x & 0xffff;
+      m[j] = sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16];
+    }
+    if (st_pending) A.wait_st();
+#pragma unroll
+    for (int j = 0; j < NDF; ++j) ai[j] = A.template ld_async<MODE>(sl[j]);
+#pragma unroll
+    for (int j = 0; j < NDF; ++j) A.wait_ld(ai[j]);
+#pragma unroll
+    for (int j = 0; j < NDF; ++j) {
+      f[j] = Rk & ~ai[j];                                           // FREE_{t,i,k} = R_k & ~A'_i
+      A.template st<MODE>(sl[j], ai[j] | Rk);                       // A'_i |= R_k
+    }
+    st_pending = true;
+  }
+  if (NDF == 3) {
+    for (int e = e0 + 3; e < e0 + ndf; ++e) {                       // more far deps (rare)
+      const int2 d = drec[e];
+      const int s = d.x & 0xffff;
+      A.wait_st();
+      uint32_t ai = A.template ld_async<MODE>(s);
+      A.wait_ld(ai);
+      A.template st<MODE>(s, ai | Rk);
+      const ET Mi = sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16];
+      for (uint32_t fx = Rk & ~ai; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
+    }
+  }
+  events<NDF + 1, ET>(Rk, sf, Mk, f, m, E, lane);
+}
+
+// Walk the quads q = q_hi .. q_lo (nodes 4q+3 .. 4q) of a group pass.
+// nrec[k] = {(int32) M_k, e0, ndf | adj << 16, slot_k or -1}.
+template <typename ET, bool TM, int MODE, bool RSTORE>
+__device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, const uint4* sn4, uint32_t* rcol,
                                      const uint32_t* brow, const int4* __restrict__ nrec,
                                      const int2* __restrict__ drec, const int64_t* __restrict__ M,
                                      const int64_t* __restrict__ C, const AView<TM>& A, ET* E, int lane,
-                                     uint4& cur, uint32_t& a_next, uint32_t& bword, uint32_t& bnext,
                                      int64_t& costL) {
-  for (int q = q_hi; q >= q_lo; --q) {
+  uint4 cur = live ? __ldcg(sn4 + q_hi) : make_uint4(0u, 0u, 0u, 0u);
+  // row 32g's word for the current 32-node block; the next block's word is prefetched
+  uint32_t bword = (g > 0 && (q_hi >> 3) < g && live) ? brow[q_hi >> 3] : 0u;
+  uint32_t bnext = (g > 0 && (q_hi >> 3) >= 1 && (q_hi >> 3) - 1 < g && live) ? brow[(q_hi >> 3) - 1] : 0u;
+  if ((q_hi & 7) == 7) bnext = bword;      // a block-aligned first quad reloads at entry
+  int4 rec1 = nrec[nk - 1];                                         // record of the next node
+  uint32_t acc = 0u;                                                // Acc_k from user k+1
+  uint32_t bslot = 0u;                                              // A'_k base when k has a slot
+  bool st_pending = true;                                           // init stores precede
+  if (rec1.w >= 0) {
+    A.wait_st();
+    bslot = A.template ld_async<MODE>(rec1.w);
+    A.wait_ld(bslot);
+    st_pending = false;
+  }
+  for (int q = q_hi; q >= 0; --q) {
     const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
     if ((q & 7) == 7) {                                             // entered a new 32-node block
       bword = bnext;
@@ -520,35 +572,82 @@ __device__ __forceinline__ void walk(int q_hi, int q_lo, int nk, int g, bool liv
     for (int u = 3; u >= 0; --u) {
       const int k = 4 * q + u;
       if (k >= nk) continue;                                        // warp-uniform
+      const int4 rec = rec1;
+      rec1 = k > 0 ? nrec[k - 1] : make_int4(0, 0, 0, -1);
+      const int64_t Ck = C[k];
       const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
+      const uint32_t sn1 = u == 3 ? cur.z : u == 2 ? cur.y : u == 1 ? cur.x : nxt.w;   // Sn_{k-1}
+      const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;           // A'_k, complete
       const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);   // S_t from S_{t+1} and row 32g
-      A.fence_st();                                                 // earlier stores visible
-      const uint32_t a = a_next;                                    // A'_k = Sn_k | Acc_k (complete)
-      a_next = k > 0 ? A.template ldm<(MODE == 1) ? 1 : MODE>(k - 1) : 0u;   // prefetch
       const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
       const uint32_t Rk = (a & ~sw) | diag;                         // a2 seed + a3 closure
-      A.template stm<MODE>(k, Rk);                                  // slot now holds R column
-      if (!__any_sync(FULL, Rk != 0u)) continue;                    // computed in no lane
-      const int4 rec = nrec[k];
-      const ET Mk = sizeof(ET) == 4 ? (ET)rec.x : (ET)M[k];
-      costL += (int64_t)__popc(Rk) * C[k];
-      const int e0 = rec.y, nd = rec.z;
-      switch (nd) {                                                 // warp-uniform
-        case 0: node_step<0, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
-        case 1: node_step<1, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
-        case 2: node_step<2, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
-        case 3: node_step<3, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
-        default: node_step<4, ET, TM, MODE>(k, Rk, a, Mk, e0, nd, drec, M, A, E, lane, a_next); break;
+      if (RSTORE && live) rcol[k] = Rk;                             // verification output
+      // base of A'_{k-1}: its slot (final: every far user j > k is done; the adjacent user k
+      // contributes through acc) or Sn_{k-1}
+      uint32_t b1 = sn1;
+      if (rec1.w >= 0) {
+        if (st_pending) { A.wait_st(); st_pending = false; }
+        b1 = A.template ld_async<MODE>(rec1.w);
       }
+      acc = 0u;
+      if (__any_sync(FULL, Rk != 0u)) {                             // computed in some lane
+        const ET Mk = sizeof(ET) == 4 ? (ET)rec.x : (ET)M[k];
+        costL += (int64_t)__popc(Rk) * Ck;
+        const bool adj = (rec.z >> 16) != 0;
+        if (rec1.w >= 0) A.wait_ld(b1);
+        const uint32_t fa = adj ? Rk & ~b1 : 0u;                    // FREE_{t,k-1,k}
+        const ET ma = sizeof(ET) == 4 ? (ET)rec1.x : (k > 0 ? (ET)M[k - 1] : (ET)0);
+        if (adj) acc = Rk;                                          // Acc_{k-1} |= R_k
+        const uint32_t sf = Rk & ~a;                                // FREE_{t,k,k}
+        const int ndf = rec.z & 0xffff;
+        switch (ndf) {                                              // warp-uniform
+          case 0: node_step<0, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
+          case 1: node_step<1, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
+          case 2: node_step<2, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
+          default: node_step<3, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
+        }
+      } else if (rec1.w >= 0) {
+        A.wait_ld(b1);
+      }
+      bslot = b1;
     }
     cur = nxt;
   }
 }
 
+// Write one 32x32 mask block set (rows 32g..32g+31 of the 32 candidates of the task) from
+// column words: col(cl, node) for candidate cl of the batch.  S: S_t words from the Sn columns
+// and row 32g (brow); R: the R columns the walk stored over the Sn columns.
+template <bool IS_S>
+__device__ void emit_mask(const ScanParams& p, uint32_t* out, int g, int nk, int64_t batch0, int lane,
+                          uint32_t* scratch) {
+  const int n = p.n, G = p.G;
+  const int W32 = 2 * ((n + 63) >> 6);
+  const int row = 32 * g + lane;
+  for (int cl = 0; cl < 32; ++cl) {
+    const int64_t cc = batch0 + cl;
+    if (cc >= p.n_cand) break;                                      // warp-uniform
+    const uint32_t* ccw = p.ws + cc * p.cs;
+    for (int w = 0; w <= g; ++w) {
+      const int node = 32 * w + lane;
+      uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
+      if (IS_S) {
+        const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
+        sc = (sc << 1) | ((bb >> lane) & 1u);
+      }
+      const uint32_t x = transpose32(sc, lane);
+      if (row < n) out[((size_t)(p.out_base + cc) * n + row) * W32 + w] = x;
+    }
+    if (row < n)
+      for (int w = g + 1; w < W32; ++w) out[((size_t)(p.out_base + cc) * n + row) * W32 + w] = 0u;
+  }
+  (void)scratch;
+}
+
 // ET = int32_t when every M is a multiple of a scale s with sum M/s < 2^30 (the host checks;
 // exact), else int64_t.  M in the blob, the masses and the results are in units of s.
-// TM: A' of nodes < 256 in Tensor Memory (8 warps, one CTA per SM, 512 TMEM columns:
-// warp w uses lane quarter w % 4 and columns 256 * (w / 4) ..).
+// TM: slots < 256 in Tensor Memory (8 warps, one CTA per SM, 512 TMEM columns: warp w uses
+// lane quarter w % 4 and columns 256 * (w / 4) ..).
 template <typename ET, bool TM>
 __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   // <= 128 regs: co-resides with K1
   extern __shared__ __align__(16) unsigned char smem[];
@@ -556,13 +655,12 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
   const int n = p.n, G = p.G;
   const int64_t* M = reinterpret_cast<const int64_t*>(smem);
   const int64_t* C = M + n;
-  const int32_t* gi = reinterpret_cast<const int32_t*>(smem + 16 * n);
   const int4* nrec = reinterpret_cast<const int4*>(smem + p.o_nrec);
   const int2* drec = reinterpret_cast<const int2*>(smem + p.o_drec);
-  (void)gi;
+  const int32_t* qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
   unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
   ET* E = reinterpret_cast<ET*>(wr);                               // [32 stages][32 lanes]
-  uint32_t* Asm = reinterpret_cast<uint32_t*>(E + 32 * 32);         // [node][lane] (spill part)
+  uint32_t* Asm = reinterpret_cast<uint32_t*>(E + 32 * 32);         // [slot][lane] (spill part)
   __shared__ uint32_t tmem_base;
   for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
@@ -577,71 +675,96 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
   AView<TM> A;
   A.sm = Asm;
   A.lane = lane;
-  A.tmc = TM ? min(p.n, 256) : 0;
+  A.tmc = TM ? min(p.n_slot, 256) : 0;
   A.taddr = TM ? tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2) : 0u;
+  const bool all_tm = TM && p.n_slot <= 256;
 
   const int tasks = G * p.n_batch;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   for (int task = gw; task < tasks; task += nwarps) {
     const int g = G - 1 - task / p.n_batch;                         // big groups first
-    const int64_t c = (int64_t)(task % p.n_batch) * 32 + lane;
+    const int64_t batch0 = (int64_t)(task % p.n_batch) * 32;
+    const int64_t c = batch0 + lane;
     const bool live = c < p.n_cand;
     const int nk = min(n, 32 * (g + 1));                            // nodes 0..nk-1
     const int nq = (nk + 3) >> 2;                                   // uint4 blocks of Sn
-    const uint32_t* cw = p.ws + (live ? c : 0) * p.cs;
+    uint32_t* cw = p.ws + (live ? c : 0) * p.cs;
     const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
-    // A'_i = Sn_i | Acc_i (Acc = OR of R over visited users): the closure reads Sn_k | Acc_k and
-    // every FREE test reads Sn_i | Acc_i, so one array serves both.  Start: A' = Sn.
+    {  // pull the warp's next task (Sn columns, row-32g words, masses) towards L2 meanwhile
+      const int tn = task + nwarps;
+      if (p.prefetch && tn < tasks) {
+        const int gn = G - 1 - tn / p.n_batch;
+        const int64_t cn = (int64_t)(tn % p.n_batch) * 32 + lane;
+        if (cn < p.n_cand) {
+          const unsigned char* b = reinterpret_cast<const unsigned char*>(p.ws + cn * p.cs);
+          const unsigned char* col = b + 4 * (size_t)grp_off(gn);
+          for (int off = 0; off < 128 * (gn + 1); off += 128) prefetch_l2(col + off);
+          prefetch_l2(col + 128 * (gn + 1) - 4);                    // the block is 16-byte aligned
+          prefetch_l2(b + 4 * ((size_t)p.brow + (size_t)gn * G));
+          const unsigned char* ms = b + 4 * (size_t)block_words(G) + 8 * (size_t)(32 * gn);
+          prefetch_l2(ms);
+          prefetch_l2(ms + 128);
+          prefetch_l2(ms + 255);
+        }
+      }
+    }
+    if (p.s_mask32) emit_mask<true>(p, p.s_mask32, g, nk, batch0, lane, nullptr);   // before R overwrites
+    // slots: A'_i = Sn_i (Acc_i = 0) for the slotted nodes of the pass.  qinfo[q] = first slot
+    // of quad q | (4-bit mask of its slotted nodes) << 16 (slots ascend with the node index).
     {  // software-pipelined: the loads of 8 quads are in flight while the previous 8 are stored
       uint4 va[8], vb[8];
+      int qa[8], qb[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) va[u] = (live && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
+      for (int u = 0; u < 8; ++u) {
+        va[u] = (live && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
+        qa[u] = u < nq ? qinfo[u] : 0;
+      }
       for (int q0 = 0; q0 < nq; q0 += 8) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 8; ++u) {
           vb[u] = (live && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
+          qb[u] = q0 + 8 + u < nq ? qinfo[q0 + 8 + u] : 0;
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i0 = 4 * (q0 + u);
           if (i0 >= nk) break;                                      // warp-uniform
-          if (TM && i0 < A.tmc) A.st4(i0, va[u]);                   // tmc % 4 == 0 or tmc == n
-          else {
-            if (i0 + 0 < nk) A.st(i0 + 0, va[u].x);
-            if (i0 + 1 < nk) A.st(i0 + 1, va[u].y);
-            if (i0 + 2 < nk) A.st(i0 + 2, va[u].z);
-            if (i0 + 3 < nk) A.st(i0 + 3, va[u].w);
+          const uint32_t wv[4] = {va[u].x, va[u].y, va[u].z, va[u].w};
+          int s = qa[u] & 0xffff;
+          const int msk = (qa[u] >> 16) & (i0 + 4 <= nk ? 15 : (1 << (nk - i0)) - 1);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if ((msk >> j) & 1) {
+              if (!TM) A.template st<0>(s, wv[j]);
+              else if (all_tm) A.template st<2>(s, wv[j]);
+              else A.template st<1>(s, wv[j]);
+              ++s;
+            }
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) va[u] = vb[u];
+        for (int u = 0; u < 8; ++u) {
+          va[u] = vb[u];
+          qa[u] = qb[u];
+        }
       }
     }
     for (int b = 0; b < 32; ++b) E[32 * b + lane] = (ET)0;
     __syncwarp();
     const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
     int64_t costL = 0;
-    uint4 cur = live ? __ldcg(sn4 + nq - 1) : make_uint4(0u, 0u, 0u, 0u);
-    A.fence_st();
-    uint32_t a_next = A.ld(nk - 1);
-    // row 32g's word for the current 32-node block; the next block's word is prefetched
-    uint32_t bword = (g > 0 && ((nq - 1) >> 3) < g && live) ? brow[(nq - 1) >> 3] : 0u;
-    uint32_t bnext = (g > 0 && ((nq - 1) >> 3) >= 1 && ((nq - 1) >> 3) - 1 < g && live)
-                         ? brow[((nq - 1) >> 3) - 1] : 0u;
-    // the first quad's block word is bword; the walk reloads bword/bnext at block entries
-    // (q & 7 == 7), so prime bnext with the current block for a block-aligned first quad
-    if (((nq - 1) & 7) == 7) bnext = bword;
-    if (!TM) {
-      walk<ET, TM, 0>(nq - 1, 0, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next, bword,
-                      bnext, costL);
+    uint32_t* rcol = cw + grp_off(g);
+    if (p.r_mask32) {
+      if (!TM) walk<ET, TM, 0, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else if (all_tm) walk<ET, TM, 2, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else walk<ET, TM, 1, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
     } else {
-      const int qb = A.tmc >> 2;                                      // quads with k >= tmc: mixed
-      if (nq - 1 >= qb)
-        walk<ET, TM, 1>(nq - 1, qb, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next, bword,
-                        bnext, costL);
-      walk<ET, TM, 2>(min(nq - 1, qb - 1), 0, nk, g, live, sn4, brow, nrec, drec, M, C, A, E, lane, cur, a_next,
-                      bword, bnext, costL);
+      if (!TM) walk<ET, TM, 0, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else if (all_tm) walk<ET, TM, 2, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else walk<ET, TM, 1, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
     }
+    A.wait_st();                                                    // next task re-fills the slots
     // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
     const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
     int64_t mv[32];
@@ -659,52 +782,15 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
       pp[0] = pk;
       pp[1] = costL;
     }
-    if (p.r_mask32 || p.s_mask32) {                                 // verification output
-      A.fence_st();
+    if (p.r_mask32) {
       __syncwarp();
-      const int W32 = 2 * ((n + 63) >> 6);
-      uint32_t* scratch = reinterpret_cast<uint32_t*>(E);             // E is dead: [32 nodes][32 lanes]
-      for (int w = 0; w <= g; ++w) {
-        for (int j = 0; j < 32; ++j) {
-          const int node = 32 * w + j;
-          scratch[32 * j + lane] = node < nk ? A.ld(node) : 0u;      // R column, own candidate
-        }
-        __syncwarp();
-        for (int cl = 0; cl < 32; ++cl) {
-          const int64_t cc = (int64_t)(task % p.n_batch) * 32 + cl;
-          if (cc >= p.n_cand) break;                                // warp-uniform
-          const uint32_t* ccw = p.ws + cc * p.cs;
-          const int row = 32 * g + lane;
-          const int node = 32 * w + lane;
-          const uint32_t rc = scratch[32 * lane + cl];
-          uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
-          const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
-          sc = (sc << 1) | ((bb >> lane) & 1u);
-          const uint32_t xr = transpose32(rc, lane);
-          const uint32_t xs = transpose32(sc, lane);
-          if (row < n) {
-            const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32;
-            if (p.r_mask32) p.r_mask32[o + w] = xr;
-            if (p.s_mask32) p.s_mask32[o + w] = xs;
-          }
-        }
-        __syncwarp();
-      }
-      const int row = 32 * g + lane;                                // zero the words above the block diagonal
-      for (int cl = 0; cl < 32; ++cl) {
-        const int64_t cc = (int64_t)(task % p.n_batch) * 32 + cl;
-        if (cc >= p.n_cand || row >= n) break;
-        const size_t o = ((size_t)(p.out_base + cc) * n + row) * W32;
-        for (int w = g + 1; w < W32; ++w) {
-          if (p.r_mask32) p.r_mask32[o + w] = 0u;
-          if (p.s_mask32) p.s_mask32[o + w] = 0u;
-        }
-      }
+      __threadfence_block();
+      emit_mask<false>(p, p.r_mask32, g, nk, batch0, lane, nullptr);
     }
     __syncwarp();
   }
   if (TM) {
-    A.fence_st();
+    A.wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
