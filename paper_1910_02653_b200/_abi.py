@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcheckmate_b200.so")
+# CM_LIB: load another build of the same library (kernel-variant tuning); never a fallback
+LIB_PATH = os.environ.get("CM_LIB") or os.path.join(_HERE, "libcheckmate_b200.so")
 
 CM_OK, CM_EINVAL, CM_ETOPO, CM_EDUP, CM_ERANGE, CM_ECUDA, CM_ENOMEM = range(7)
 CM_NMAX = 1024

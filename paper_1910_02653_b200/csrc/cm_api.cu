@@ -63,10 +63,6 @@ int kernel_choice() {                 // CM_KERNEL=v1 selects the row-form kerne
   const char* e = std::getenv("CM_KERNEL");
   return (e && std::strcmp(e, "v1") == 0) ? 1 : 2;
 }
-int cpw_override() {
-  const char* e = std::getenv("CM_CPW");
-  return e ? std::atoi(e) : 0;
-}
 constexpr int64_t kDefaultWsBytes = int64_t(512) << 20;  // two 256 MB chunk buffers: ~6 waves of scan tasks per chunk
 }  // namespace
 
@@ -171,8 +167,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   int occ1 = 0, occ2 = 0;
-  const int nt_max = std::min(4, a->n_theta);
-  const size_t smem1 = cm2::k1_smem_bytes(nt_max, g->d_nib32 ? g->nib_entries : 0);
+  const int nib_staged = g->d_nib32 ? g->nib_entries : 0;
+  auto smem1_for = [&](int nt) { return cm2::k1_smem_bytes(nt, nib_staged); };
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     static bool carve = false;
@@ -183,7 +179,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                              reinterpret_cast<const void*>(cm2::round_tma_kernel<3>),
                              reinterpret_cast<const void*>(cm2::round_tma_kernel<4>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)cm2::k1_smem_bytes(4, 128 * 32));
+                                 (int)std::max(cm2::k1_smem_bytes(1, 128 * 32), cm2::k1_smem_bytes(4, 128 * 32)));
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(round_tma_kernel)");
@@ -215,7 +211,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
-  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel<4>, 256, smem1);
+  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel<4>, 256, smem1_for(4));
   else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_ldg_kernel, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
@@ -288,19 +284,22 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     rp.s_count = sc;
     rp.sn = blk;
     const int64_t warps1 = use_tma ? (int64_t)sc : (int64_t)sc * G;   // TMA K1: a task is one S*
-    // one K1 CTA per SM (8 warps, 64 KB, 32k registers): it co-resides with the scan CTA
-    // (TMEM variant: 8 warps, ~144 KB, 32k registers), so chunk c+1 streams while c scans.
-    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + 7) / 8, (int64_t)g->sm_count));
+    // one K1 CTA per SM (<= 32k registers): it co-resides with the scan CTA (TMEM variant:
+    // 8 warps, 32k registers), so chunk c+1 streams while c scans.
     if (tr) cudaEventRecord(trace_event(4 * c + 0), g->st_round);
     for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
       rp.th0 = th0;
       rp.nt = std::min(4, a->n_theta - th0);
+      const int wpb = use_tma ? cm2::k1_warps(rp.nt) : 8;
+      const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + wpb - 1) / wpb, (int64_t)g->sm_count));
+      const int thr1 = 32 * wpb;
       if (use_tma) {
+        const size_t sm1 = smem1_for(rp.nt);
         switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
-          case 2: cm2::round_tma_kernel<2><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
-          case 3: cm2::round_tma_kernel<3><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
-          default: cm2::round_tma_kernel<4><<<grid1, 256, smem1, g->st_round>>>(rp, tmap); break;
+          case 1: cm2::round_tma_kernel<1><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 2: cm2::round_tma_kernel<2><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 3: cm2::round_tma_kernel<3><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          default: cm2::round_tma_kernel<4><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
         }
       } else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
     }
@@ -309,6 +308,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_round[b], 0);
     if (e != cudaSuccess) break;
     if (tr) cudaEventRecord(trace_event(4 * c + 2), st);
+#ifdef CM_EXP_NOK2
+    e = cudaEventRecord(g->ev_scan[b], st);
+    g->used[b] = true;
+    continue;
+#endif
     sp.ws = blk;
     sp.n_cand = nc;
     sp.n_batch = (int)((nc + 31) / 32);

@@ -173,16 +173,26 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
 // the strict lower triangle, stores them, and transposes them into row words for the row's
 // checkpoint mass mass_r = sum_{i in S_r} M_i (the Eq. 6 sum, from 4-bit
 // tables) and for row 32(g+1)'s word (the brow operand of K2).
-constexpr int kStages = 2;     // 64 KB per CTA: co-resides with the TMEM scan CTA (144 KB)
-constexpr int kK1Warps = 8;
-// Shared layout (bytes from a 1024-aligned base): tiles, mbarriers, NT column-word slots per
-// warp (one per threshold, so the NT chains interleave), then the staged int32 mass tables.
-struct K1Smem {
-  float tile[kK1Warps][kStages][32][32];      // 4 KB tiles, 1024-byte aligned (swizzle atom)
-  uint64_t bar[kK1Warps][kStages];
-};
-__host__ __device__ constexpr size_t k1_cols_off() { return sizeof(K1Smem); }
-__host__ __device__ constexpr size_t k1_nib_off(int nt) { return sizeof(K1Smem) + (size_t)kK1Warps * nt * 128; }
+// Warps per CTA, TMA stages per warp and the register cap depend on NT: with one threshold
+// K1 runs 12 warps x 3 stages at <= 80 registers (30k registers, ~150 KB), so it still
+// co-resides with the TMEM scan CTA (8 warps x 128 registers, ~50 KB) while hiding more latency.
+#ifndef CM_K1_WARPS1
+#define CM_K1_WARPS1 8
+#endif
+#ifndef CM_K1_STAGES1
+#define CM_K1_STAGES1 2
+#endif
+#ifndef CM_K1_REGS1
+#define CM_K1_REGS1 128
+#endif
+__host__ __device__ constexpr int k1_warps(int nt) { return nt == 1 ? CM_K1_WARPS1 : 8; }
+__host__ __device__ constexpr int k1_stages(int nt) { return nt == 1 ? CM_K1_STAGES1 : 2; }
+// Shared layout (bytes from a 1024-aligned base): tiles [warp][stage][32][32] f32 (4 KB each,
+// 1024-byte aligned: the swizzle atom), mbarriers [warp][stage], NT column-word slots per warp
+// (one per threshold, so the NT chains interleave), then the staged int32 mass tables.
+__host__ __device__ constexpr size_t k1_bar_off(int nt) { return (size_t)k1_warps(nt) * k1_stages(nt) * 4096; }
+__host__ __device__ constexpr size_t k1_cols_off(int nt) { return k1_bar_off(nt) + (size_t)k1_warps(nt) * k1_stages(nt) * 8; }
+__host__ __device__ constexpr size_t k1_nib_off(int nt) { return k1_cols_off(nt) + (size_t)k1_warps(nt) * nt * 128; }
 // dynamic bytes to request: + 1024 slack for aligning the base
 __host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries) {
   return k1_nib_off(nt) + 4 * (size_t)nib_entries + 1024;
@@ -191,20 +201,26 @@ __host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries) {
 // NT = thresholds per pass (1..4, a compile-time count so the per-threshold work of one block
 // -- ballots, mass lookups, transposes -- forms NT independent instruction chains).
 template <int NT>
-__global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int kSt = k1_stages(NT);
   extern __shared__ __align__(1024) unsigned char k1raw[];
   unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
-  K1Smem& sm = *reinterpret_cast<K1Smem*>(k1smem);
   int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT));   // p.nib32 staged (if any)
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  uint32_t(*cols_w)[32] = reinterpret_cast<uint32_t(*)[32]>(k1smem + k1_cols_off()) + NT * wl;
+  float(*tiles)[32][32] = reinterpret_cast<float(*)[32][32]>(k1smem) + kSt * wl;   // [stage]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k1smem + k1_bar_off(NT)) + kSt * wl;
+  uint32_t(*cols_w)[32] = reinterpret_cast<uint32_t(*)[32]>(k1smem + k1_cols_off(NT)) + NT * wl;
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
   const int G = p.G;
+  // row groups with a row r = 32g+1+l < n; the Sn columns of later groups are all zero
+  // (S_{n+1} = 0) and K2 does not read them
+  const int Gr = p.n >= 2 ? (p.n - 2) / 32 + 1 : 0;
+  if (Gr == 0) return;
   if (p.nib32)
     for (int i = threadIdx.x; i < p.nib_entries; i += blockDim.x) nib32[i] = p.nib32[i];
   if (lane == 0)
-    for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wl][st], 1);
+    for (int st = 0; st < kSt; ++st) mbar_init(&bars[st], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   float th[NT];
@@ -212,38 +228,36 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
   for (int j = 0; j < NT; ++j) th[j] = p.theta[p.th0 + j];
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
-  const uint32_t row_base = smem_u32(&sm.tile[wl][0][lane][0]);     // stage 0, this lane's row
+  const uint32_t row_base = smem_u32(&tiles[0][lane][0]);            // stage 0, this lane's row
   const uint64_t pol = p.evict_first ? l2_evict_first_policy() : 0ull;
   const uint32_t swz = (uint32_t)(lane & 7) << 4;
 
-  // Producer cursor (ps, pg, pw) runs kStages-1 blocks ahead of the consumer.  No proxy
+  // Producer cursor (ps, pg, pw) runs kSt-1 blocks ahead of the consumer.  No proxy
   // fence before re-filling a stage: its previous contents were consumed (ballots issued on
   // the loaded values, then __syncwarp) before the refill is issued.
   int ps = wid, pg = 0, pw = 0, pstage = 0;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
     if (lane == 0) {
-      mbar_expect_tx(&sm.bar[wl][pstage], 32u * 32u * 4u);
+      mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
       if (pol)
-        tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
-                    &sm.bar[wl][pstage], pol);
+        tma_load_3d(&tiles[pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
       else
-        tma_load_3d(&sm.tile[wl][pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps),
-                    &sm.bar[wl][pstage]);
+        tma_load_3d(&tiles[pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
     }
-    pstage = pstage + 1 == kStages ? 0 : pstage + 1;
+    pstage = pstage + 1 == kSt ? 0 : pstage + 1;
     if (++pw > pg) {
       pw = 0;
-      if (++pg == G) { pg = 0; ps += nw; }
+      if (++pg == Gr) { pg = 0; ps += nw; }
     }
   };
-  for (int d = 0; d < kStages - 1; ++d) issue();
+  for (int d = 0; d < kSt - 1; ++d) issue();
 
   int cstage = 0;
   uint32_t phase_bits = 0u;                                         // bit st = parity of stage st
   for (int s = wid; s < p.s_count; s += nw) {
     uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
       // rows of the group that exist (r < n): bits [0, hi)
       const int hi = p.n - 1 - 32 * g;
@@ -253,7 +267,7 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
       for (int j = 0; j < NT; ++j) mass[j] = 0;
       for (int w = 0; w <= g; ++w) {
         issue();
-        mbar_wait(&sm.bar[wl][cstage], (phase_bits >> cstage) & 1u);
+        mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
         const uint32_t rb = row_base + (uint32_t)cstage * (32u * 32u * 4u);
         float x[32];
@@ -264,7 +278,7 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
                        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + (((uint32_t)c << 4) ^ swz)));
           x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
         }
-        cstage = cstage + 1 == kStages ? 0 : cstage + 1;
+        cstage = cstage + 1 == kSt ? 0 : cstage + 1;
 #pragma unroll
         for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -284,10 +298,16 @@ __global__ void __maxnreg__(128) round_tma_kernel(const RoundParams p, const __g
         for (int j = 0; j < NT; ++j) {
           uint32_t* oj = out + (int64_t)j * p.cs;
           oj[grp_off(g) + node] = word[j];
+#ifndef CM_EXP_NOMASS
           word[j] = transpose(word[j]);                             // row rq's word over block w
+#endif
           if (lane == 31 && g + 1 < G) oj[brow_at] = word[j];
         }
+#ifdef CM_EXP_NOMASS
+        if (false) {
+#else
         if (scaled32) {                                             // scaled masses fit int32
+#endif
           const unsigned char* tb = reinterpret_cast<const unsigned char*>(nib32 + 128 * w);
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
@@ -461,34 +481,44 @@ struct AView {
 // Events of one computing node k: for every stage bit b of R_k (stage b computes k), in the
 // backward walk, first the frees at k (Eq. 9: the masks f_j with masses m_j, and the i = k
 // self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k.  NM dependency
-// masks (compile-time), up to four stage bits per round (their loads issue together).
+// masks (compile-time).  A round takes up to W stage bits of x (their loads issue together);
+// the width follows the warp's largest per-lane event count (REDUX), so nodes whose lanes
+// compute in one or two stages do not pay for four-wide rounds.
+template <int W, int NM, typename ET>
+__device__ __forceinline__ void event_round(uint32_t& x, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
+                                            ET* E, int lane) {
+  int b[W];
+  bool v[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    v[u] = x != 0u;
+    b[u] = v[u] ? __ffs(x) - 1 : 0;
+    x &= x - 1;
+  }
+  ET ev[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) ev[u] = v[u] ? E[32 * b[u] + lane] : (ET)0;
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    if ((sf >> b[u]) & 1u) ev[u] -= Mk;
+#pragma unroll
+    for (int j = 0; j < NM; ++j)
+      if ((f[j] >> b[u]) & 1u) ev[u] -= m[j];
+    ev[u] = (ev[u] > 0 ? ev[u] : (ET)0) + Mk;
+  }
+#pragma unroll
+  for (int u = 0; u < W; ++u)
+    if (v[u]) E[32 * b[u] + lane] = ev[u];
+}
 template <int NM, typename ET>
 __device__ __forceinline__ void events(uint32_t Rk, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
                                        ET* E, int lane) {
-  for (uint32_t x = Rk; x;) {
-    int b[4];
-    bool v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      v[u] = x != 0u;
-      b[u] = v[u] ? __ffs(x) - 1 : 0;
-      x &= x - 1;
-    }
-    ET ev[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) ev[u] = v[u] ? E[32 * b[u] + lane] : (ET)0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if ((sf >> b[u]) & 1u) ev[u] -= Mk;
-#pragma unroll
-      for (int j = 0; j < NM; ++j)
-        if ((f[j] >> b[u]) & 1u) ev[u] -= m[j];
-      ev[u] = (ev[u] > 0 ? ev[u] : (ET)0) + Mk;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (v[u]) E[32 * b[u] + lane] = ev[u];
-  }
+  const unsigned mx = __reduce_max_sync(FULL, (unsigned)__popc(Rk));
+  uint32_t x = Rk;
+  if (mx <= 1) event_round<1, NM, ET>(x, sf, Mk, f, m, E, lane);
+  else if (mx == 2) event_round<2, NM, ET>(x, sf, Mk, f, m, E, lane);
+  else
+    while (__any_sync(FULL, x != 0u)) event_round<4, NM, ET>(x, sf, Mk, f, m, E, lane);
 }
 
 // The far (non-adjacent) dependencies of node k (NDF of them; NDF = 3 also walks any further
@@ -541,12 +571,12 @@ __device__ __forceinline__ void node_step(uint32_t Rk, uint32_t sf, ET Mk, uint3
 // Walk the quads q = q_hi .. q_lo (nodes 4q+3 .. 4q) of a group pass.
 // nrec[k] = {(int32) M_k, e0, ndf | adj << 16, slot_k or -1}.
 template <typename ET, bool TM, int MODE, bool RSTORE>
-__device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, const uint4* sn4, uint32_t* rcol,
+__device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, bool lsn, const uint4* sn4, uint32_t* rcol,
                                      const uint32_t* brow, const int4* __restrict__ nrec,
                                      const int2* __restrict__ drec, const int64_t* __restrict__ M,
                                      const int64_t* __restrict__ C, const AView<TM>& A, ET* E, int lane,
                                      int64_t& costL) {
-  uint4 cur = live ? __ldcg(sn4 + q_hi) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 cur = lsn ? __ldcg(sn4 + q_hi) : make_uint4(0u, 0u, 0u, 0u);
   // row 32g's word for the current 32-node block; the next block's word is prefetched
   uint32_t bword = (g > 0 && (q_hi >> 3) < g && live) ? brow[q_hi >> 3] : 0u;
   uint32_t bnext = (g > 0 && (q_hi >> 3) >= 1 && (q_hi >> 3) - 1 < g && live) ? brow[(q_hi >> 3) - 1] : 0u;
@@ -562,7 +592,7 @@ __device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, const u
     st_pending = false;
   }
   for (int q = q_hi; q >= 0; --q) {
-    const uint4 nxt = (q > 0 && live) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4 nxt = (q > 0 && lsn) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
     if ((q & 7) == 7) {                                             // entered a new 32-node block
       bword = bnext;
       const int wb = (q >> 3) - 1;
@@ -630,7 +660,7 @@ __device__ void emit_mask(const ScanParams& p, uint32_t* out, int g, int nk, int
     const uint32_t* ccw = p.ws + cc * p.cs;
     for (int w = 0; w <= g; ++w) {
       const int node = 32 * w + lane;
-      uint32_t sc = node < nk ? ccw[grp_off(g) + node] : 0u;
+      uint32_t sc = node < nk && (!IS_S || 32 * g + 1 < n) ? ccw[grp_off(g) + node] : 0u;
       if (IS_S) {
         const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
         sc = (sc << 1) | ((bb >> lane) & 1u);
@@ -691,6 +721,7 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
     const int nq = (nk + 3) >> 2;                                   // uint4 blocks of Sn
     uint32_t* cw = p.ws + (live ? c : 0) * p.cs;
     const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
+    const bool lsn = live && 32 * g + 1 < n;                        // K1 wrote Sn for this group
     {  // pull the warp's next task (Sn columns, row-32g words, masses) towards L2 meanwhile
       const int tn = task + nwarps;
       if (p.prefetch && tn < tasks) {
@@ -699,8 +730,10 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
         if (cn < p.n_cand) {
           const unsigned char* b = reinterpret_cast<const unsigned char*>(p.ws + cn * p.cs);
           const unsigned char* col = b + 4 * (size_t)grp_off(gn);
-          for (int off = 0; off < 128 * (gn + 1); off += 128) prefetch_l2(col + off);
-          prefetch_l2(col + 128 * (gn + 1) - 4);                    // the block is 16-byte aligned
+          if (32 * gn + 1 < n) {                                    // the group has Sn columns
+            for (int off = 0; off < 128 * (gn + 1); off += 128) prefetch_l2(col + off);
+            prefetch_l2(col + 128 * (gn + 1) - 4);                  // the block is 16-byte aligned
+          }
           prefetch_l2(b + 4 * ((size_t)p.brow + (size_t)gn * G));
           const unsigned char* ms = b + 4 * (size_t)block_words(G) + 8 * (size_t)(32 * gn);
           prefetch_l2(ms);
@@ -717,13 +750,13 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
       int qa[8], qb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        va[u] = (live && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
+        va[u] = (lsn && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
         qa[u] = u < nq ? qinfo[u] : 0;
       }
       for (int q0 = 0; q0 < nq; q0 += 8) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          vb[u] = (live && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
+          vb[u] = (lsn && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
           qb[u] = q0 + 8 + u < nq ? qinfo[q0 + 8 + u] : 0;
         }
 #pragma unroll
@@ -756,13 +789,13 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
     int64_t costL = 0;
     uint32_t* rcol = cw + grp_off(g);
     if (p.r_mask32) {
-      if (!TM) walk<ET, TM, 0, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else if (all_tm) walk<ET, TM, 2, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else walk<ET, TM, 1, true>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      if (!TM) walk<ET, TM, 0, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else if (all_tm) walk<ET, TM, 2, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else walk<ET, TM, 1, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
     } else {
-      if (!TM) walk<ET, TM, 0, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else if (all_tm) walk<ET, TM, 2, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else walk<ET, TM, 1, false>(nq - 1, nk, g, live, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      if (!TM) walk<ET, TM, 0, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else if (all_tm) walk<ET, TM, 2, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+      else walk<ET, TM, 1, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
     }
     A.wait_st();                                                    // next task re-fills the slots
     // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
