@@ -476,6 +476,12 @@ struct AView {
   __device__ __forceinline__ void wait_st() const {
     if (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
+  // slots s..s+3, all in TMEM (TM, s + 3 < tmc)
+  __device__ __forceinline__ void st4(int s, uint4 v) const {
+    if (TM)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+                   :: "r"(taddr + (uint32_t)s), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+  }
 };
 
 // Events of one computing node k: for every stage bit b of R_k (stage b computes k), in the
@@ -766,6 +772,10 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
           const uint32_t wv[4] = {va[u].x, va[u].y, va[u].z, va[u].w};
           int s = qa[u] & 0xffff;
           const int msk = (qa[u] >> 16) & (i0 + 4 <= nk ? 15 : (1 << (nk - i0)) - 1);
+          if (msk == 15 && all_tm) {                                // four consecutive slots
+            A.st4(s, va[u]);
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             if ((msk >> j) & 1) {
