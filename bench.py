@@ -82,11 +82,14 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def load_traffic(cfg):
+def load_traffic(cfg, batch):
+    """DRAM bytes (read + write) of one step, from the committed ncu --set full capture
+    (profiles/traffic.json: bytes per S* of K1+K2+K3 for a config), scaled to the batch."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get(cfg)
+        d = json.load(open(p)).get(cfg)
+        if d:
+            return d["dram_bytes_per_sstar"] * batch
     return None
 
 
@@ -343,6 +346,7 @@ def main():
     # one extra traced step (untimed): per-chunk K1 (a1 stream, internal stream) and K2+K3
     # (scan + reduce, caller stream) event times, for the per-kernel breakdown
     kernels = None
+    launches = None
     try:
         os.environ["CM_TRACE"] = "1"
         step()
@@ -352,13 +356,15 @@ def main():
         k1 = sum(t[1] - t[0] for t in tr)
         k2 = sum(t[3] - t[2] for t in tr)
         span = max(t[3] for t in tr) - min(t[0] for t in tr)
+        # our kernels per step: per chunk ceil(n_theta/4) K1 launches + K2 + K3
+        launches = a.steps * len(tr) * ((n_theta + 3) // 4 + 2)
         kernels = {"chunks": len(tr), "k1_round_ms": k1, "k2_scan_reduce_ms": k2, "span_ms": span,
                    "k1_hbm_gbs": alg_bytes / (k1 / 1000.0) / 1e9,
                    "k1_frac": alg_bytes / (k1 / 1000.0) / 1e9 / peak_gbs,
                    "overlap": "K1(chunk c+1) runs on an internal stream concurrently with K2(chunk c)"}
     except Exception as ex:  # pragma: no cover
         kernels = {"error": str(ex)}
-    traffic = load_traffic(a.config)
+    traffic = load_traffic(a.config, batch)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
             "frac": achieved / peak_gbs, "traffic": traffic,
             "kernel": "whole a1-a7 path per step (K1 TMA round + K2 TMEM scan + K3 reduce, overlapped)",
@@ -375,7 +381,7 @@ def main():
                        "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
                        "parallelism": f"candidates sharded over {world} GPU(s), NCCL MIN all-reduce of keys",
                        "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush"},
-            "gpu_launches": a.steps, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks,
             "best": [cm.decode_key(k, cm.key_idx_bits(total)) for k in best]}
     print(json.dumps(line), flush=True)
