@@ -120,6 +120,10 @@ void cm_decode_key(int64_t key, int32_t idx_bits, int64_t* cost, int64_t* idx);
  * to the first k1_begin, into out[max_values] and returns the count written (0 if none). */
 int32_t cm_debug_trace(float* out, int32_t max_values);
 
+/* Debug aid: the number of kernels the calling thread's last cm_round_and_evaluate launched
+ * (1 on the fused persistent path; per chunk ceil(n_theta/4) + 2 on the two-kernel pipeline). */
+int32_t cm_debug_last_launches(void);
+
 const char* cm_status_string(cm_status s);
 const char* cm_last_error(void);
 

@@ -103,6 +103,11 @@ def debug_trace(max_values: int = 4096):
     return [tuple(buf[i:i + 4]) for i in range(0, m, 4)]
 
 
+
+def debug_last_launches() -> int:
+    """Kernels launched by this thread's last round_and_evaluate call (cm_debug_last_launches)."""
+    return int(_lib.cm_debug_last_launches())
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 

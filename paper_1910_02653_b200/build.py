@@ -40,20 +40,43 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> list:
+def _compile_one(src, obj, inc):
+    cmd = [NVCC] + ARCH + [f for f in FLAGS if f != "-shared"] + inc + ["-c", "-o", obj, src]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return cmd, r
+
+
+def build(force: bool = False, verbose: bool = False, extra=None, out_override=None) -> list:
+    """Each .cu is compiled to an object in parallel (the kernel instances live in their own
+    translation units), then linked into the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
     built = []
     for out, (srcs, hdrs, inc) in LIBS.items():
-        if not force and not _stale(out, srcs + hdrs):
+        if out_override and out.endswith("libcheckmate_b200.so"):
+            out = out_override
+        elif out_override:
             continue
-        cmd = [NVCC] + ARCH + FLAGS + inc + ["-o", out] + srcs
+        if not force and not extra and not _stale(out, srcs + hdrs):
+            continue
+        inc = inc + list(extra or [])
+        objdir = os.path.join(os.path.dirname(out), "build", os.path.basename(out))
+        os.makedirs(objdir, exist_ok=True)
+        objs = [os.path.join(objdir, os.path.basename(sf) + ".o") for sf in srcs]
+        with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
+            res = list(ex.map(lambda a: _compile_one(*a), [(sf, ob, inc) for sf, ob in zip(srcs, objs)]))
+        logs = []
+        for cmd, r in res:
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+            logs.append(r.stdout + r.stderr)
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", out] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {out}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-        log = out + ".ptxas.txt"
-        with open(log, "w") as f:
-            f.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc link failed for {out}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        with open(out + ".ptxas.txt", "w") as f:
+            f.write("".join(logs))
         if verbose:
-            print(r.stdout + r.stderr)
+            print("".join(logs))
         built.append(out)
     return built
 

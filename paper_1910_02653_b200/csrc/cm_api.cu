@@ -13,7 +13,8 @@
 
 #include "cm.h"
 #include "cm_kernel.cuh"
-#include "cm_v2.cuh"
+#define CM_API_TU
+#include "cm_inst.cuh"
 
 namespace {
 
@@ -100,6 +101,7 @@ struct Trace {
   int used = 0;
 };
 Trace g_trace;
+thread_local int32_t g_launches = 0;   // kernels launched by this thread's last cm_round_and_evaluate
 bool trace_enabled() {
   const char* e = std::getenv("CM_TRACE");
   return e && std::strcmp(e, "1") == 0;
@@ -122,6 +124,20 @@ bool tmem_enabled() {
 int env_flag(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
+}
+
+// L2 sector promotion of the K1 tensor-map loads.  A block row is 128 bytes; a 256-byte
+// promotion also pulls the next 32 nodes of the row (for the diagonal block w = g, entries of
+// the never-read upper triangle), yet it measured fastest once rows are 128-byte aligned
+// (ld % 32 == 0): 12.97 vs 12.63 M cand/s (128 B) at n = 353 in the two-kernel pipeline.
+// CM_L2PROMO = 0 / 64 / 128 / 256 (tuning), default 256 (measured best with 128-byte aligned rows).
+CUtensorMapL2promotion l2_promotion() {
+  switch (env_flag("CM_L2PROMO", 256)) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
 }
 
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
@@ -168,18 +184,23 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   }
   int occ1 = 0, occ2 = 0;
   const int nib_staged = g->d_nib32 ? g->nib_entries : 0;
-  auto smem1_for = [&](int nt) { return cm2::k1_smem_bytes(nt, nib_staged); };
+  const bool bulk = a->layout == CM_LAYOUT_TRI4;                    // K1 by 1-D bulk copies (tri4) or tensor-map TMA
+  auto smem1_for = [&](int nt) { return cm2::k1_smem_bytes(nt, nib_staged, bulk); };
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
-      for (const void* fn : {reinterpret_cast<const void*>(cm2::round_tma_kernel<1>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4>)}) {
+      for (const void* fn : {reinterpret_cast<const void*>(cm2::round_tma_kernel<1, false>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2, false>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3, false>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4, false>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<1, true>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2, true>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3, true>),
+                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4, true>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(cm2::k1_smem_bytes(1, 128 * 32), cm2::k1_smem_bytes(4, 128 * 32)));
+                                 (int)std::max(cm2::k1_smem_bytes(1, 128 * 32, true), cm2::k1_smem_bytes(4, 128 * 32, true)));
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(round_tma_kernel)");
@@ -187,8 +208,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
-                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>),
-                             reinterpret_cast<const void*>(cm2::round_ldg_kernel)}) {
+                             reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>)}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
@@ -208,11 +228,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
-  if (use_tma) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_tma_kernel<4>, 256, smem1_for(4));
-  else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cm2::round_ldg_kernel, 256, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, bulk ? cm2::round_tma_kernel<4, true> : cm2::round_tma_kernel<4, false>,
+                                                    256, smem1_for(4));
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
@@ -264,11 +284,90 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   qp.cost = a->cost;
   qp.best_key = a->best_key;
 
+  // ---- fused persistent path (one launch; see cm2::fused_kernel) ----
+  if (g->scan32 && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
+    const int nt = a->n_theta;
+    const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
+    const size_t smemf = k1b + fixed + wb * cm2::kFusedScanWarps + 1024;
+    const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n);
+    const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
+    const int64_t total_tasks = (units - 1) * (int64_t)G * nt +
+                                (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
+    int64_t ring_max = env_flag("CM_RING", 512);   // measured: 64 -> 5.8, 256 -> 14.4, 512+ -> 14.8 M cand/s
+    int64_t R = std::min<int64_t>(ring_max, units);
+    auto ctl_bytes = [](int64_t r) { return (4 * (2 + 3 * r) + 255) & ~int64_t(255); };
+    while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
+    if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= ws_bytes &&
+        total_tasks < (int64_t(1) << 31)) {
+      const void* fn = nullptr;
+      switch (nt * 2 + (bulk ? 1 : 0)) {
+        case 2: fn = reinterpret_cast<const void*>(cm2::fused_kernel<1, false>); break;
+        case 3: fn = reinterpret_cast<const void*>(cm2::fused_kernel<1, true>); break;
+        case 4: fn = reinterpret_cast<const void*>(cm2::fused_kernel<2, false>); break;
+        case 5: fn = reinterpret_cast<const void*>(cm2::fused_kernel<2, true>); break;
+        case 6: fn = reinterpret_cast<const void*>(cm2::fused_kernel<3, false>); break;
+        case 7: fn = reinterpret_cast<const void*>(cm2::fused_kernel<3, true>); break;
+        case 8: fn = reinterpret_cast<const void*>(cm2::fused_kernel<4, false>); break;
+        default: fn = reinterpret_cast<const void*>(cm2::fused_kernel<4, true>); break;
+      }
+      {
+        std::lock_guard<std::mutex> lock(attr_mu);
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fused_kernel)");
+      }
+      const int threads = 32 * cm2::fused_warps(nt);
+      int occf = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, fn, threads, smemf);
+      if (e != cudaSuccess) return cuda_fail(e, "occupancy(fused_kernel)");
+      if (occf >= 1) {
+        cm2::FusedParams fp;
+        rp.s_begin = 0;
+        rp.s_count = a->n_sstar;
+        rp.th0 = 0;
+        rp.nt = nt;
+        rp.sn = nullptr;
+        fp.rp = rp;
+        fp.sp = sp;
+        fp.qp = qp;
+        uint32_t* ctl = reinterpret_cast<uint32_t*>(ws);
+        fp.ctl = ctl;
+        fp.ring = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + ctl_bytes(R));
+        fp.slot_words = slot_bytes / 4;
+        fp.n_slots = (int32_t)R;
+        fp.n_sstar = a->n_sstar;
+        fp.n_theta = nt;
+        fp.n_units = (int32_t)units;
+        fp.tpu = G * nt;
+        fp.total_tasks = total_tasks;
+        std::lock_guard<std::mutex> lock(g->mu);
+        e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
+        if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
+        void* args[] = {&fp, &tmap};
+        const bool tr = trace_enabled();
+        g_trace.used = 0;
+        if (tr) cudaEventRecord(trace_event(0), st);
+        e = cudaLaunchKernel(fn, dim3((unsigned)g->sm_count), dim3((unsigned)threads), args, smemf, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch fused_kernel");
+        if (tr) {                                    // one "chunk": K1 and K2 share the launch
+          cudaEventRecord(trace_event(1), st);
+          cudaEventRecord(trace_event(2), st);
+          cudaEventRecord(trace_event(3), st);
+          g_trace.used = 4;
+        }
+        g_launches = 1;
+        return CM_OK;
+      }
+    }
+  }
+
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   const int64_t half = cap * cand_bytes(n);
   std::lock_guard<std::mutex> lock(g->mu);
   const bool tr = trace_enabled();
   g_trace.used = 0;
+  g_launches = 0;
   e = cudaEventRecord(g->ev_start, st);                       // inputs written on `st` before the call
   if (e == cudaSuccess) e = cudaStreamWaitEvent(g->st_round, g->ev_start, 0);
   int c = 0;
@@ -283,25 +382,36 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     rp.s_begin = s0;
     rp.s_count = sc;
     rp.sn = blk;
-    const int64_t warps1 = use_tma ? (int64_t)sc : (int64_t)sc * G;   // TMA K1: a task is one S*
+    const int64_t warps1 = sc;                                   // a K1 task is one S*
     // one K1 CTA per SM (<= 32k registers): it co-resides with the scan CTA (TMEM variant:
     // 8 warps, 32k registers), so chunk c+1 streams while c scans.
     if (tr) cudaEventRecord(trace_event(4 * c + 0), g->st_round);
+#ifdef CM_EXP_NOK1
+    for (int th0 = 0; th0 < 0; th0 += 4) {                    // timing experiment: no rounding
+#else
     for (int th0 = 0; th0 < a->n_theta; th0 += 4) {          // <= 4 thresholds per S* pass
+#endif
       rp.th0 = th0;
       rp.nt = std::min(4, a->n_theta - th0);
-      const int wpb = use_tma ? cm2::k1_warps(rp.nt) : 8;
+      const int wpb = cm2::k1_warps(rp.nt);
       const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + wpb - 1) / wpb, (int64_t)g->sm_count));
       const int thr1 = 32 * wpb;
-      if (use_tma) {
-        const size_t sm1 = smem1_for(rp.nt);
+      const size_t sm1 = smem1_for(rp.nt);
+      if (bulk) {
         switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 2: cm2::round_tma_kernel<2><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 3: cm2::round_tma_kernel<3><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          default: cm2::round_tma_kernel<4><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 1: cm2::round_tma_kernel<1, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 2: cm2::round_tma_kernel<2, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 3: cm2::round_tma_kernel<3, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          default: cm2::round_tma_kernel<4, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
         }
-      } else cm2::round_ldg_kernel<<<grid1, 256, 0, g->st_round>>>(rp);
+      } else {
+        switch (rp.nt) {
+          case 1: cm2::round_tma_kernel<1, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 2: cm2::round_tma_kernel<2, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 3: cm2::round_tma_kernel<3, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          default: cm2::round_tma_kernel<4, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+        }
+      }
     }
     if (tr) cudaEventRecord(trace_event(4 * c + 1), g->st_round);
     e = cudaEventRecord(g->ev_round[b], g->st_round);
@@ -332,7 +442,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     qp.part = part;
     qp.n_cand = nc;
     qp.out_base = sp.out_base;
-    cm2::reduce_kernel<<<(int)((nc + 255) / 256), 256, 0, st>>>(qp);
+    cm2::reduce_kernel<0><<<(int)((nc + 255) / 256), 256, 0, st>>>(qp);
+    g_launches += (a->n_theta + 3) / 4 + 2;
     if (tr) {
       cudaEventRecord(trace_event(4 * c + 3), st);
       g_trace.used = 4 * (c + 1);
@@ -628,6 +739,8 @@ int32_t cm_debug_trace(float* out, int32_t max_values) {
   return m;
 }
 
+int32_t cm_debug_last_launches(void) { return g_launches; }
+
 int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {
   if (!g || chunk_candidates < 1) return -1;
   return 2 * cand_bytes(g->n) * ((chunk_candidates + 31) & ~int64_t(31));   // two buffers
@@ -652,8 +765,10 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (a->n_sstar > 0) {
     if (a->sstar_stride < min_stride || (a->sstar_stride & 3))
       return fail(CM_EINVAL, "sstar_stride too small or not a multiple of 4");
-    if (!a->sstar || (reinterpret_cast<uintptr_t>(a->sstar) & 15))
+    // n = 1 has no strict-lower entries: nothing is read, sstar may be NULL (an empty tri4 batch)
+    if (min_stride > 0 && (!a->sstar || (reinterpret_cast<uintptr_t>(a->sstar) & 15)))
       return fail(CM_EINVAL, "sstar NULL or not 16-byte aligned");
+    if (!a->sstar && n > 1) return fail(CM_EINVAL, "sstar NULL");
     if (!a->theta || !a->peak || !a->cost) return fail(CM_EINVAL, "NULL theta/peak/cost");
   }
   if (a->n_budget > 0 && (!a->budget || !a->best_key)) return fail(CM_EINVAL, "NULL budget/best_key");
@@ -664,6 +779,7 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   const int32_t idx_bits = cm_key_idx_bits(a->total_candidates);
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
+  g_launches = 0;
   if (n_cand == 0) return CM_OK;
   if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(g->n_slot, g->scan32, false) <= (size_t)g->smem_optin) {
     cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
@@ -737,6 +853,7 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   p.s_mask = a->s_mask;
   p.tri_words = tri_words;
   cmk::round_evaluate_kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  g_launches = 1;
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "launch round_evaluate_kernel");
   return CM_OK;

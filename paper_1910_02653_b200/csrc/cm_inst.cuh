@@ -1,0 +1,18 @@
+// cm_inst.cuh -- the kernel instances.  Each is compiled in its own translation unit
+// (k_*.cu, built in parallel); the API translation unit only refers to them.
+#pragma once
+#include "cm_v2.cuh"
+
+#define CM_ROUND(NT, BULK) template __global__ void cm2::round_tma_kernel<NT, BULK>(const cm2::RoundParams, const __grid_constant__ CUtensorMap);
+#define CM_SCAN(ET, TM) template __global__ void cm2::scan_kernel<ET, TM>(const cm2::ScanParams);
+#define CM_FUSED(NT, BULK) template __global__ void cm2::fused_kernel<NT, BULK>(const cm2::FusedParams, const __grid_constant__ CUtensorMap);
+#define CM_REDUCE template __global__ void cm2::reduce_kernel<0>(const cm2::ReduceParams);
+
+#ifdef CM_API_TU
+extern CM_ROUND(1, false) extern CM_ROUND(2, false) extern CM_ROUND(3, false) extern CM_ROUND(4, false)
+extern CM_ROUND(1, true) extern CM_ROUND(2, true) extern CM_ROUND(3, true) extern CM_ROUND(4, true)
+extern CM_SCAN(int32_t, false) extern CM_SCAN(int32_t, true) extern CM_SCAN(int64_t, false) extern CM_SCAN(int64_t, true)
+extern CM_FUSED(1, false) extern CM_FUSED(1, true) extern CM_FUSED(2, false) extern CM_FUSED(2, true)
+extern CM_FUSED(3, false) extern CM_FUSED(3, true) extern CM_FUSED(4, false) extern CM_FUSED(4, true)
+extern CM_REDUCE
+#endif

@@ -159,6 +159,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, 
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
       :: "r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
 }
+// 1-D bulk copy global -> shared (SASS UBLKCP): `bytes` % 16 == 0, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(ptr));
 }
@@ -190,78 +196,144 @@ __host__ __device__ constexpr int k1_stages(int nt) { return nt == 1 ? CM_K1_STA
 // Shared layout (bytes from a 1024-aligned base): tiles [warp][stage][32][32] f32 (4 KB each,
 // 1024-byte aligned: the swizzle atom), mbarriers [warp][stage], NT column-word slots per warp
 // (one per threshold, so the NT chains interleave), then the staged int32 mass tables.
-__host__ __device__ constexpr size_t k1_bar_off(int nt) { return (size_t)k1_warps(nt) * k1_stages(nt) * 4096; }
-__host__ __device__ constexpr size_t k1_cols_off(int nt) { return k1_bar_off(nt) + (size_t)k1_warps(nt) * k1_stages(nt) * 8; }
-__host__ __device__ constexpr size_t k1_nib_off(int nt) { return k1_cols_off(nt) + (size_t)k1_warps(nt) * nt * 128; }
+// A stage holds one 32 x 32 block.  TMA (dense): 4 KB, 128-byte swizzled rows.  BULK (tri4):
+// rows at a 144-byte pitch (one 16-byte chunk of skew per row), so lane l reading 16-byte
+// chunk c of its row hits bank group (l + c) % 8: conflict-free without a swizzle.
+constexpr int kBulkPitch = 144;
+__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 32 * kBulkPitch : 4096; }
+__host__ __device__ constexpr size_t k1_bar_off(int nt, bool bulk = false) {
+  return ((size_t)k1_warps(nt) * k1_stages(nt) * k1_stage_bytes(bulk) + 1023) & ~(size_t)1023;
+}
+__host__ __device__ constexpr size_t k1_cols_off(int nt, bool bulk = false) {
+  return k1_bar_off(nt, bulk) + (size_t)k1_warps(nt) * k1_stages(nt) * 8;
+}
+__host__ __device__ constexpr size_t k1_nib_off(int nt, bool bulk = false) {
+  return k1_cols_off(nt, bulk) + (size_t)k1_warps(nt) * nt * 128;
+}
 // dynamic bytes to request: + 1024 slack for aligning the base
-__host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries) {
-  return k1_nib_off(nt) + 4 * (size_t)nib_entries + 1024;
+__host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries, bool bulk = false) {
+  return k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1024;
 }
 
 // NT = thresholds per pass (1..4, a compile-time count so the per-threshold work of one block
 // -- ballots, mass lookups, transposes -- forms NT independent instruction chains).
-template <int NT>
-__global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+// BULK = false: dense layout, one 3-D tensor-map TMA per block (rows >= n zero-filled, 128-byte
+// swizzle).  BULK = true: packed tri4 layout (row r at the float offset sum_{r'<r} roundup4(r'),
+// not an affine map, so no tensor map): lane l issues one 1-D bulk copy of its own row's
+// segment, nodes 32w .. min(32w+32, roundup4(r))-1 -- exactly the stored strict-lower entries
+// (plus < 4 floats of row padding), so the HBM stream is the algorithmic one.  Rows >= n are
+// not copied; whatever a stage holds outside the copied segments is masked away below (cmask).
+// Where K1 writes candidate block (S* s, threshold th0 + j): begin(s) gives the block of
+// threshold th0 (blocks of one S* are consecutive, cs words each) and end(s) runs after every
+// word of S* s is written.  K1Plain: the chunk buffer of the two-kernel pipeline.
+// first() / next(s) give the S* a warp processes, in order (K1Plain: a static stride).
+struct K1Plain {
+  uint32_t* sn;
+  int32_t n_theta, th0, cs;
+  int32_t wid, nw;
+  __device__ __forceinline__ int first() const { return wid; }
+  __device__ __forceinline__ int next(int s) const { return s + nw; }
+  __device__ __forceinline__ uint32_t* begin(int s) const { return sn + ((int64_t)s * n_theta + th0) * cs; }
+  __device__ __forceinline__ void end(int) const {}
+};
+
+// Per-CTA K1 set-up (staged mass table, mbarriers); the caller synchronises the CTA after it.
+template <int NT, bool BULK>
+__device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1smem, int nwarps1, int tid,
+                                         int nthreads) {
   constexpr int kSt = k1_stages(NT);
-  extern __shared__ __align__(1024) unsigned char k1raw[];
-  unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
-  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT));   // p.nib32 staged (if any)
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  float(*tiles)[32][32] = reinterpret_cast<float(*)[32][32]>(k1smem) + kSt * wl;   // [stage]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(k1smem + k1_bar_off(NT)) + kSt * wl;
-  uint32_t(*cols_w)[32] = reinterpret_cast<uint32_t(*)[32]>(k1smem + k1_cols_off(NT)) + NT * wl;
-  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT, BULK));
+  if (p.nib32)
+    for (int i = tid; i < p.nib_entries; i += nthreads) nib32[i] = p.nib32[i];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k1smem + k1_bar_off(NT, BULK));
+  if (tid < nwarps1 * kSt) mbar_init(&bars[tid], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// K1 body of one warp: S* s = hk.first(), hk.next(s), ... while < s_count; wl = the warp's
+// index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
+// consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
+// takes queue in `sq` (8 per warp) until the consumer reaches them.
+template <int NT, bool BULK, class Hooks>
+__device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, unsigned char* k1smem,
+                                        int wl, int* sq, const Hooks& hk) {
+  constexpr int kSt = k1_stages(NT);
+  constexpr uint32_t kStageBytes = (uint32_t)k1_stage_bytes(BULK);
+  int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT, BULK));   // p.nib32 staged (if any)
+  const int lane = threadIdx.x & 31;
+  unsigned char* tiles = k1smem + (size_t)kSt * kStageBytes * wl;                   // [stage] of this warp
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k1smem + k1_bar_off(NT, BULK)) + kSt * wl;
   const int G = p.G;
   // row groups with a row r = 32g+1+l < n; the Sn columns of later groups are all zero
   // (S_{n+1} = 0) and K2 does not read them
   const int Gr = p.n >= 2 ? (p.n - 2) / 32 + 1 : 0;
-  if (Gr == 0) return;
-  if (p.nib32)
-    for (int i = threadIdx.x; i < p.nib_entries; i += blockDim.x) nib32[i] = p.nib32[i];
-  if (lane == 0)
-    for (int st = 0; st < kSt; ++st) mbar_init(&bars[st], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
+  if (Gr == 0) {
+    for (int s = hk.first(); s < p.s_count; s = hk.next(s)) { hk.begin(s); hk.end(s); }
+    return;
+  }
   float th[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) th[j] = p.theta[p.th0 + j];
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
-  const uint32_t row_base = smem_u32(&tiles[0][lane][0]);            // stage 0, this lane's row
-  const uint64_t pol = p.evict_first ? l2_evict_first_policy() : 0ull;
-  const uint32_t swz = (uint32_t)(lane & 7) << 4;
+  const uint32_t tiles_u32 = smem_u32(tiles);
+  const uint32_t row_base = tiles_u32 + (uint32_t)lane * (BULK ? (uint32_t)kBulkPitch : 128u);   // stage 0, this lane's row
+  const uint64_t pol = (!BULK && p.evict_first) ? l2_evict_first_policy() : 0ull;
+  const uint32_t swz = BULK ? 0u : (uint32_t)(lane & 7) << 4;
 
   // Producer cursor (ps, pg, pw) runs kSt-1 blocks ahead of the consumer.  No proxy
   // fence before re-filling a stage: its previous contents were consumed (ballots issued on
   // the loaded values, then __syncwarp) before the refill is issued.
-  int ps = wid, pg = 0, pw = 0, pstage = 0;
+  int ps = hk.first(), pg = 0, pw = 0, pstage = 0;
+  unsigned qhead = 0, qtail = 0;                                    // sq ring (warp-uniform)
+  if (lane == 0) sq[0] = ps;
+  ++qhead;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
-    if (lane == 0) {
+    if (BULK) {
+      // this lane's row r = 32 pg + 1 + lane, nodes 32 pw .. : the stored part of the block
+      const int r = 32 * pg + 1 + lane;
+      const int len = r < p.n ? min(32, ((r + 3) & ~3) - 32 * pw) : 0;   // floats, % 4 == 0, > 0 if r < n
+      const uint32_t total = __reduce_add_sync(FULL, (uint32_t)len) * 4u;
+      if (lane == 0) mbar_expect_tx(&bars[pstage], total);
+      __syncwarp();
+      if (len > 0) {
+        const float* src = p.sstar + (p.s_begin + ps) * p.stride + row_offset(1, 0, r) + 32 * pw;
+        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)lane * kBulkPitch, src, 4u * (uint32_t)len,
+                  &bars[pstage]);
+      }
+    } else if (lane == 0) {
       mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
+      void* dst = tiles + (size_t)pstage * kStageBytes;
       if (pol)
-        tma_load_3d(&tiles[pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
+        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
       else
-        tma_load_3d(&tiles[pstage][0][0], &tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
+        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
     }
     pstage = pstage + 1 == kSt ? 0 : pstage + 1;
     if (++pw > pg) {
       pw = 0;
-      if (++pg == Gr) { pg = 0; ps += nw; }
+      if (++pg == Gr) {
+        pg = 0;
+        ps = hk.next(ps);
+        if (lane == 0) sq[qhead & 7] = ps;
+        ++qhead;
+      }
     }
   };
   for (int d = 0; d < kSt - 1; ++d) issue();
 
   int cstage = 0;
   uint32_t phase_bits = 0u;                                         // bit st = parity of stage st
-  for (int s = wid; s < p.s_count; s += nw) {
-    uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
+  for (;;) {
+    __syncwarp();
+    const int s = sq[qtail & 7];
+    ++qtail;
+    if (s >= p.s_count) break;
+    uint32_t* out = hk.begin(s);
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
       // rows of the group that exist (r < n): bits [0, hi)
-      const int hi = p.n - 1 - 32 * g;
-      const uint32_t rows_ok = hi >= 32 ? FULL : (hi <= 0 ? 0u : (1u << hi) - 1u);
       int64_t mass[NT];
 #pragma unroll
       for (int j = 0; j < NT; ++j) mass[j] = 0;
@@ -269,7 +341,7 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
         issue();
         mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
-        const uint32_t rb = row_base + (uint32_t)cstage * (32u * 32u * 4u);
+        const uint32_t rb = row_base + (uint32_t)cstage * kStageBytes;
         float x[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -279,35 +351,28 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
           x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
         }
         cstage = cstage + 1 == kSt ? 0 : cstage + 1;
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-          for (int q = 0; q < 32; ++q) cols_w[j][q] = __ballot_sync(FULL, x[q] > th[j]);
-        __syncwarp();                                               // tile read, ballots stored
-        // Column mask of node i = 32w + lane: rows r = 32g+1+b with i < r (strict lower
-        // triangle: b >= 32(w-g) + lane) and r < n.  Zero-filled / upper entries never leak.
-        const int lo = 32 * (w - g) + lane;
-        const uint32_t cmask = rows_ok & (lo <= 0 ? FULL : (lo >= 32 ? 0u : FULL << lo));
+        // Row word of this lane's row r = rq over block w: bit q = S_{r, 32w+q} = [x_q > theta]
+        // (a1: strict fp32 '>', NaN -> 0), masked to the strict lower triangle (32w+q < r) and
+        // to rows r < n, so zero-filled or stale stage contents never leak.
+        const int rem = rq - 32 * w;                                // >= 1: nodes 32w .. rq-1 exist
+        const uint32_t rmask = rq >= p.n ? 0u : (rem >= 32 ? FULL : (1u << rem) - 1u);
         uint32_t word[NT];
 #pragma unroll
-        for (int j = 0; j < NT; ++j) word[j] = cols_w[j][lane] & cmask;   // node i's column
-        __syncwarp();
+        for (int j = 0; j < NT; ++j) {
+          uint32_t rw = 0u;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) rw |= x[q] > th[j] ? (1u << q) : 0u;
+          word[j] = rw & rmask;
+        }
         const int node = 32 * w + lane;
-        const int brow_at = p.brow + (g + 1) * G + w;               // row 32(g+1)'s word (lane 31)
+        const int brow_at = p.brow + (g + 1) * G + w;               // row 32(g+1) = lane 31's row
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           uint32_t* oj = out + (int64_t)j * p.cs;
-          oj[grp_off(g) + node] = word[j];
-#ifndef CM_EXP_NOMASS
-          word[j] = transpose(word[j]);                             // row rq's word over block w
-#endif
           if (lane == 31 && g + 1 < G) oj[brow_at] = word[j];
+          oj[grp_off(g) + node] = transpose(word[j]);               // node 32w+lane's column: bit b = row 32g+1+b
         }
-#ifdef CM_EXP_NOMASS
-        if (false) {
-#else
         if (scaled32) {                                             // scaled masses fit int32
-#endif
           const unsigned char* tb = reinterpret_cast<const unsigned char*>(nib32 + 128 * w);
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
@@ -335,80 +400,22 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
         for (int j = 0; j < NT; ++j) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
       }
     }
+    hk.end(s);
   }
 }
 
-// K1 for the packed tri4 layout (rows of irregular stride).  Per task (S*, g) the warp covers rows r_q = 32g+1+q, q = 0..31 (the S_{t+1} rows of the
-// group's stages), 32 nodes (block w) at a time.  Lane = node: row q of the block is one
-// coalesced 128-byte load, one compare (a1, strict fp32 '>', NaN -> 0) and one ballot, which
-// is already the packed row word.  The 32 row words go through a 32-word shared slot to
-// lane q, which transposes them into column words and adds the checkpoint mass of its
-// row, mass_r = sum_{i in S_r} M_i (the Eq. 6 sum), from 4-bit tables.
-// Out-of-triangle elements are replaced by NaN, which compares false for every theta.
-__global__ void __launch_bounds__(256) round_ldg_kernel(const RoundParams p) {
-  __shared__ uint32_t rows_w[8][32];                              // per-warp ballot slot
-  __shared__ int64_t rows_off[8][32];                             // per-warp row offsets
-  const int64_t* nib = p.nib;
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
-  const int tasks = p.s_count * p.G;
-  const float qnan = __int_as_float(0x7fffffff);
-  for (int task = wid; task < tasks; task += nw) {
-    const int s = task / p.G;
-    const int g = task - s * p.G;
-    const float* S0 = p.sstar + (p.s_begin + s) * p.stride;
-    uint32_t* out = p.sn + ((int64_t)s * p.n_theta + p.th0) * p.cs;
-    const int rq = 32 * g + lane + 1;                               // row owned by this lane
-    rows_off[wl][lane] = row_offset(p.layout, p.ld, rq);
-    __syncwarp();
-    const bool full_rows = (32 * g + 32) < p.n;                     // every r_q exists
-    int64_t mass[4] = {0, 0, 0, 0};
-    for (int w = 0; w <= g; ++w) {
-      const int node = 32 * w + lane;
-      float x[32];
-      if (w < g && full_rows) {                                     // interior block: no masking
-#pragma unroll
-        for (int q = 0; q < 32; ++q) x[q] = __ldcs(S0 + rows_off[wl][q] + node);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int r = 32 * g + 1 + q;
-          x[q] = (r < p.n && node < r) ? __ldcs(S0 + rows_off[wl][q] + node) : qnan;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j >= p.nt) break;
-        const float th = __ldg(p.theta + p.th0 + j);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const uint32_t b = __ballot_sync(FULL, x[q] > th);
-          rows_w[wl][q] = b;                                        // uniform value: one store
-        }
-        __syncwarp();
-        const uint32_t word = rows_w[wl][lane];                     // row r_q's word, block w
-        __syncwarp();
-        int64_t ms = 0;
-        if (word) {
-          const int64_t* tw = nib + 128 * w;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) ms += __ldg(tw + 16 * q + ((word >> (4 * q)) & 15u));
-        }
-        uint32_t* oj = out + (int64_t)j * p.cs;
-        if (lane == 31 && g + 1 < p.G) oj[p.brow + (g + 1) * p.G + w] = word;   // row 32(g+1)
-        oj[grp_off(g) + node] = transpose32(word, lane);
-        mass[j] += ms;
-      }
-    }
-    if (rq < p.n) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < p.nt) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
-    }
-    __syncwarp();
-  }
+template <int NT, bool BULK>
+__global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char k1raw[];
+  unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
+  k1_setup<NT, BULK>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
+  __syncthreads();
+  __shared__ int sq[32][8];
+  const K1Plain hk{p.sn, p.n_theta, p.th0, p.cs, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
+                   (int)((gridDim.x * blockDim.x) >> 5)};
+  k1_body<NT, BULK>(p, &tmap, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
 }
+
 
 // ------------------------------------------------------------------------------------ K2
 // Group-major scan: a task is (stage group g, 32 candidates); lane l works on candidate
@@ -466,6 +473,9 @@ struct AView {
   __device__ __forceinline__ void wait_ld(uint32_t& v) const {
     if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
   }
+  __device__ __forceinline__ void wait_ld3(uint32_t& v0, uint32_t& v1, uint32_t& v2) const {
+    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v0), "+r"(v1), "+r"(v2) :: "memory");
+  }
   template <int MODE>
   __device__ __forceinline__ void st(int s, uint32_t v) const {
     if (in_tmem<MODE>(s))
@@ -484,110 +494,120 @@ struct AView {
   }
 };
 
-// Events of one computing node k: for every stage bit b of R_k (stage b computes k), in the
+// Events of one computing node k: for every stage bit b of x (stage b computes k), in the
 // backward walk, first the frees at k (Eq. 9: the masks f_j with masses m_j, and the i = k
-// self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k.  NM dependency
-// masks (compile-time).  A round takes up to W stage bits of x (their loads issue together);
-// the width follows the warp's largest per-lane event count (REDUX), so nodes whose lanes
-// compute in one or two stages do not pay for four-wide rounds.
+// self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k, written as
+// max(E_b - frees + M_k, M_k).  NM dependency masks (compile-time).  A round takes up to W
+// stage bits of x, highest first (FLO yields the index; stages are independent, so the order
+// is free), and their loads issue together; the width follows the warp's largest per-lane
+// event count (REDUX), so nodes whose lanes compute in one or two stages do not pay for
+// four-wide rounds.  x excludes the diagonal stage t = k: that compute is the first event of
+// stage t in the walk (R_{t,k} = 0 for k > t), so it always leaves E_t = M_t and the scan
+// initialises E with it instead.
 template <int W, int NM, typename ET>
 __device__ __forceinline__ void event_round(uint32_t& x, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
                                             ET* E, int lane) {
-  int b[W];
-  bool v[W];
+  uint32_t sel[W];
+  int off[W];
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    v[u] = x != 0u;
-    b[u] = v[u] ? __ffs(x) - 1 : 0;
-    x &= x - 1;
+    const int b = 31 - __clz(x);                                    // -1 when x == 0
+    sel[u] = x != 0u ? 1u << b : 0u;
+    off[u] = 32 * (b & 31) + lane;
+    x ^= sel[u];
   }
   ET ev[W];
 #pragma unroll
-  for (int u = 0; u < W; ++u) ev[u] = v[u] ? E[32 * b[u] + lane] : (ET)0;
+  for (int u = 0; u < W; ++u) ev[u] = sel[u] ? E[off[u]] : (ET)0;
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    if ((sf >> b[u]) & 1u) ev[u] -= Mk;
+    ET fr = (sf & sel[u]) ? Mk : (ET)0;
 #pragma unroll
     for (int j = 0; j < NM; ++j)
-      if ((f[j] >> b[u]) & 1u) ev[u] -= m[j];
-    ev[u] = (ev[u] > 0 ? ev[u] : (ET)0) + Mk;
+      if (f[j] & sel[u]) fr += m[j];
+    ev[u] = max(ev[u] - fr + Mk, Mk);
   }
 #pragma unroll
   for (int u = 0; u < W; ++u)
-    if (v[u]) E[32 * b[u] + lane] = ev[u];
+    if (sel[u]) E[off[u]] = ev[u];
 }
 template <int NM, typename ET>
-__device__ __forceinline__ void events(uint32_t Rk, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
+__device__ __forceinline__ void events(uint32_t x, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
                                        ET* E, int lane) {
-  const unsigned mx = __reduce_max_sync(FULL, (unsigned)__popc(Rk));
-  uint32_t x = Rk;
-  if (mx <= 1) event_round<1, NM, ET>(x, sf, Mk, f, m, E, lane);
+  const unsigned mx = __reduce_max_sync(FULL, (unsigned)__popc(x));
+  if (mx == 0) return;
+  if (mx == 1) event_round<1, NM, ET>(x, sf, Mk, f, m, E, lane);
   else if (mx == 2) event_round<2, NM, ET>(x, sf, Mk, f, m, E, lane);
   else
     while (__any_sync(FULL, x != 0u)) event_round<4, NM, ET>(x, sf, Mk, f, m, E, lane);
 }
 
-// The far (non-adjacent) dependencies of node k (NDF of them; NDF = 3 also walks any further
-// ones, applying their frees first), the adjacent one (mask fa, mass ma; zero when absent),
-// then the events.  drec[e] = {slot_i | i << 16, (int32) M_i}.
-template <int NDF, typename ET, bool TM, int MODE>
-__device__ __forceinline__ void node_step(uint32_t Rk, uint32_t sf, ET Mk, uint32_t fa, ET ma, int e0, int ndf,
-                                          const int2* __restrict__ drec, const int64_t* __restrict__ M,
+// The far (non-adjacent) dependencies of node k (ndf of them, warp-uniform; three in
+// registers, any further ones applied first in a rare loop), the adjacent one (mask fa, mass
+// ma; zero when absent), then the events.  drec[e] = {slot_i | i << 16, (int32) M_i}.
+// One body for every ndf: the walk's hot loop must stay small (instruction-cache resident
+// next to the rounding code on the same SM).
+template <typename ET, bool TM, int MODE>
+__device__ __forceinline__ void node_step(uint32_t Rk, uint32_t diag, uint32_t sf, ET Mk, uint32_t fa, ET ma, int e0,
+                                          int ndf, const int2* __restrict__ drec, const int64_t* __restrict__ M,
                                           const AView<TM>& A, ET* E, int lane, bool& st_pending) {
-  uint32_t f[NDF + 1];
-  ET m[NDF + 1];
-  f[NDF] = fa;
-  m[NDF] = ma;
-  if (NDF > 0) {
-    int sl[NDF > 0 ? NDF : 1];
-    uint32_t ai[NDF > 0 ? NDF : 1];
+  if (ndf == 0) {
+    events<1, ET>(Rk & ~diag, sf, Mk, &fa, &ma, E, lane);
+    return;
+  }
+  uint32_t f[4] = {0u, 0u, 0u, fa};
+  ET m[4] = {(ET)0, (ET)0, (ET)0, ma};
+  int sl[3] = {0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < NDF; ++j) {
+  for (int j = 0; j < 3; ++j)
+    if (j < ndf) {
       const int2 d = drec[e0 + j];
       sl[j] = d.x & 0xffff;
       m[j] = sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16];
     }
-    if (st_pending) A.wait_st();
+  if (st_pending) A.wait_st();
+  uint32_t ai[3] = {0u, 0u, 0u};
 #pragma unroll
-    for (int j = 0; j < NDF; ++j) ai[j] = A.template ld_async<MODE>(sl[j]);
+  for (int j = 0; j < 3; ++j)
+    if (j < ndf) ai[j] = A.template ld_async<MODE>(sl[j]);
+  A.wait_ld3(ai[0], ai[1], ai[2]);
 #pragma unroll
-    for (int j = 0; j < NDF; ++j) A.wait_ld(ai[j]);
-#pragma unroll
-    for (int j = 0; j < NDF; ++j) {
+  for (int j = 0; j < 3; ++j)
+    if (j < ndf) {
       f[j] = Rk & ~ai[j];                                           // FREE_{t,i,k} = R_k & ~A'_i
       A.template st<MODE>(sl[j], ai[j] | Rk);                       // A'_i |= R_k
     }
-    st_pending = true;
+  st_pending = true;
+  for (int e = e0 + 3; e < e0 + ndf; ++e) {                         // more far deps (rare)
+    const int2 d = drec[e];
+    const int s = d.x & 0xffff;
+    A.wait_st();
+    uint32_t ai1 = A.template ld_async<MODE>(s);
+    A.wait_ld(ai1);
+    A.template st<MODE>(s, ai1 | Rk);
+    const ET Mi = sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16];
+    for (uint32_t fx = Rk & ~ai1 & ~diag; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
   }
-  if (NDF == 3) {
-    for (int e = e0 + 3; e < e0 + ndf; ++e) {                       // more far deps (rare)
-      const int2 d = drec[e];
-      const int s = d.x & 0xffff;
-      A.wait_st();
-      uint32_t ai = A.template ld_async<MODE>(s);
-      A.wait_ld(ai);
-      A.template st<MODE>(s, ai | Rk);
-      const ET Mi = sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16];
-      for (uint32_t fx = Rk & ~ai; fx; fx &= fx - 1) E[32 * (__ffs(fx) - 1) + lane] -= Mi;
-    }
-  }
-  events<NDF + 1, ET>(Rk, sf, Mk, f, m, E, lane);
+  events<4, ET>(Rk & ~diag, sf, Mk, f, m, E, lane);
 }
 
-// Walk the quads q = q_hi .. q_lo (nodes 4q+3 .. 4q) of a group pass.
+// Walk the nodes k = nk-1 .. 0 of a group pass, one node per iteration.
 // nrec[k] = {(int32) M_k, e0, ndf | adj << 16, slot_k or -1}.
 template <typename ET, bool TM, int MODE, bool RSTORE>
-__device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, bool lsn, const uint4* sn4, uint32_t* rcol,
+__device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const uint4* sn4, uint32_t* rcol,
                                      const uint32_t* brow, const int4* __restrict__ nrec,
                                      const int2* __restrict__ drec, const int64_t* __restrict__ M,
                                      const int64_t* __restrict__ C, const AView<TM>& A, ET* E, int lane,
                                      int64_t& costL) {
-  uint4 cur = lsn ? __ldcg(sn4 + q_hi) : make_uint4(0u, 0u, 0u, 0u);
-  // row 32g's word for the current 32-node block; the next block's word is prefetched
-  uint32_t bword = (g > 0 && (q_hi >> 3) < g && live) ? brow[q_hi >> 3] : 0u;
-  uint32_t bnext = (g > 0 && (q_hi >> 3) >= 1 && (q_hi >> 3) - 1 < g && live) ? brow[(q_hi >> 3) - 1] : 0u;
-  if ((q_hi & 7) == 7) bnext = bword;      // a block-aligned first quad reloads at entry
-  int4 rec1 = nrec[nk - 1];                                         // record of the next node
+  const int k0 = nk - 1;
+  // Sn words of the quad holding k and of the quad below (for Sn_{k-1}), loaded a quad ahead
+  uint4 quad = lsn ? __ldcg(sn4 + (k0 >> 2)) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 nquad = (lsn && (k0 >> 2) > 0) ? __ldcg(sn4 + (k0 >> 2) - 1) : make_uint4(0u, 0u, 0u, 0u);
+  // row 32g's word for k's 32-node block (blocks w < g only; nodes >= 32g are never in S_32g)
+  // and, prefetched, for the block below
+  uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
+  uint32_t bnext = (g > 0 && (k0 >> 5) >= 1 && live) ? __ldcg(brow + (k0 >> 5) - 1) : 0u;
+  int4 rec1 = nrec[k0];                                             // record of the next node
   uint32_t acc = 0u;                                                // Acc_k from user k+1
   uint32_t bslot = 0u;                                              // A'_k base when k has a slot
   bool st_pending = true;                                           // init stores precede
@@ -597,57 +617,49 @@ __device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, bool ls
     A.wait_ld(bslot);
     st_pending = false;
   }
-  for (int q = q_hi; q >= 0; --q) {
-    const uint4 nxt = (q > 0 && lsn) ? __ldcg(sn4 + q - 1) : make_uint4(0u, 0u, 0u, 0u);
-    if ((q & 7) == 7) {                                             // entered a new 32-node block
+#pragma unroll 1
+  for (int k = k0; k >= 0; --k) {
+    const int u = k & 3;
+    const int4 rec = rec1;
+    rec1 = k > 0 ? nrec[k - 1] : make_int4(0, 0, 0, -1);
+    const int64_t Ck = C[k];
+    const uint32_t sn = u == 3 ? quad.w : u == 2 ? quad.z : u == 1 ? quad.y : quad.x;
+    const uint32_t sn1 = u == 3 ? quad.z : u == 2 ? quad.y : u == 1 ? quad.x : nquad.w;   // Sn_{k-1}
+    const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;             // A'_k, complete
+    const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);     // S_t from S_{t+1} and row 32g
+    const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
+    const uint32_t Rk = (a & ~sw) | diag;                           // a2 seed + a3 closure
+    if (RSTORE && live) rcol[k] = Rk;                               // verification output
+    // base of A'_{k-1}: its slot (final: every far user j > k is done; the adjacent user k
+    // contributes through acc) or Sn_{k-1}
+    uint32_t b1 = sn1;
+    if (rec1.w >= 0) {
+      if (st_pending) { A.wait_st(); st_pending = false; }
+      b1 = A.template ld_async<MODE>(rec1.w);
+    }
+    acc = 0u;
+    if (__any_sync(FULL, Rk != 0u)) {                               // computed in some lane
+      const ET Mk = sizeof(ET) == 4 ? (ET)rec.x : (ET)M[k];
+      costL += (int64_t)__popc(Rk) * Ck;
+      const bool adj = (rec.z >> 16) != 0;
+      if (rec1.w >= 0) A.wait_ld(b1);
+      const uint32_t fa = adj ? Rk & ~b1 : 0u;                      // FREE_{t,k-1,k}
+      const ET ma = sizeof(ET) == 4 ? (ET)rec1.x : (k > 0 ? (ET)M[k - 1] : (ET)0);
+      if (adj) acc = Rk;                                            // Acc_{k-1} |= R_k
+      const uint32_t sf = Rk & ~a;                                  // FREE_{t,k,k}
+      node_step<ET, TM, MODE>(Rk, diag, sf, Mk, fa, ma, rec.y, rec.z & 0xffff, drec, M, A, E, lane, st_pending);
+    } else if (rec1.w >= 0) {
+      A.wait_ld(b1);
+    }
+    bslot = b1;
+    if (u == 0) {                                                   // next node is in the quad below
+      quad = nquad;
+      nquad = (lsn && (k >> 2) >= 2) ? __ldcg(sn4 + (k >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    if ((k & 31) == 0) {                                            // next node is in the block below
       bword = bnext;
-      const int wb = (q >> 3) - 1;
-      bnext = (g > 0 && wb >= 0 && wb < g && live) ? brow[wb] : 0u;
+      bnext = (g > 0 && (k >> 5) >= 2 && live) ? __ldcg(brow + (k >> 5) - 2) : 0u;
     }
-#pragma unroll
-    for (int u = 3; u >= 0; --u) {
-      const int k = 4 * q + u;
-      if (k >= nk) continue;                                        // warp-uniform
-      const int4 rec = rec1;
-      rec1 = k > 0 ? nrec[k - 1] : make_int4(0, 0, 0, -1);
-      const int64_t Ck = C[k];
-      const uint32_t sn = u == 3 ? cur.w : u == 2 ? cur.z : u == 1 ? cur.y : cur.x;
-      const uint32_t sn1 = u == 3 ? cur.z : u == 2 ? cur.y : u == 1 ? cur.x : nxt.w;   // Sn_{k-1}
-      const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;           // A'_k, complete
-      const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);   // S_t from S_{t+1} and row 32g
-      const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
-      const uint32_t Rk = (a & ~sw) | diag;                         // a2 seed + a3 closure
-      if (RSTORE && live) rcol[k] = Rk;                             // verification output
-      // base of A'_{k-1}: its slot (final: every far user j > k is done; the adjacent user k
-      // contributes through acc) or Sn_{k-1}
-      uint32_t b1 = sn1;
-      if (rec1.w >= 0) {
-        if (st_pending) { A.wait_st(); st_pending = false; }
-        b1 = A.template ld_async<MODE>(rec1.w);
-      }
-      acc = 0u;
-      if (__any_sync(FULL, Rk != 0u)) {                             // computed in some lane
-        const ET Mk = sizeof(ET) == 4 ? (ET)rec.x : (ET)M[k];
-        costL += (int64_t)__popc(Rk) * Ck;
-        const bool adj = (rec.z >> 16) != 0;
-        if (rec1.w >= 0) A.wait_ld(b1);
-        const uint32_t fa = adj ? Rk & ~b1 : 0u;                    // FREE_{t,k-1,k}
-        const ET ma = sizeof(ET) == 4 ? (ET)rec1.x : (k > 0 ? (ET)M[k - 1] : (ET)0);
-        if (adj) acc = Rk;                                          // Acc_{k-1} |= R_k
-        const uint32_t sf = Rk & ~a;                                // FREE_{t,k,k}
-        const int ndf = rec.z & 0xffff;
-        switch (ndf) {                                              // warp-uniform
-          case 0: node_step<0, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
-          case 1: node_step<1, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
-          case 2: node_step<2, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
-          default: node_step<3, ET, TM, MODE>(Rk, sf, Mk, fa, ma, rec.y, ndf, drec, M, A, E, lane, st_pending); break;
-        }
-      } else if (rec1.w >= 0) {
-        A.wait_ld(b1);
-      }
-      bslot = b1;
-    }
-    cur = nxt;
   }
 }
 
@@ -655,29 +667,190 @@ __device__ __forceinline__ void walk(int q_hi, int nk, int g, bool live, bool ls
 // column words: col(cl, node) for candidate cl of the batch.  S: S_t words from the Sn columns
 // and row 32g (brow); R: the R columns the walk stored over the Sn columns.
 template <bool IS_S>
-__device__ void emit_mask(const ScanParams& p, uint32_t* out, int g, int nk, int64_t batch0, int lane,
-                          uint32_t* scratch) {
+__device__ void emit_mask(const ScanParams& p, const uint32_t* ws, int64_t n_cand, int64_t out_base, uint32_t* out,
+                          int g, int nk, int64_t batch0, int lane) {
   const int n = p.n, G = p.G;
   const int W32 = 2 * ((n + 63) >> 6);
   const int row = 32 * g + lane;
   for (int cl = 0; cl < 32; ++cl) {
     const int64_t cc = batch0 + cl;
-    if (cc >= p.n_cand) break;                                      // warp-uniform
-    const uint32_t* ccw = p.ws + cc * p.cs;
+    if (cc >= n_cand) break;                                        // warp-uniform
+    const uint32_t* ccw = ws + cc * p.cs;
     for (int w = 0; w <= g; ++w) {
       const int node = 32 * w + lane;
-      uint32_t sc = node < nk && (!IS_S || 32 * g + 1 < n) ? ccw[grp_off(g) + node] : 0u;
+      uint32_t sc = node < nk && (!IS_S || 32 * g + 1 < n) ? __ldcg(ccw + grp_off(g) + node) : 0u;
       if (IS_S) {
-        const uint32_t bb = (g > 0 && w < g) ? ccw[p.brow + g * G + w] : 0u;
+        const uint32_t bb = (g > 0 && w < g) ? __ldcg(ccw + p.brow + g * G + w) : 0u;
         sc = (sc << 1) | ((bb >> lane) & 1u);
       }
       const uint32_t x = transpose32(sc, lane);
-      if (row < n) out[((size_t)(p.out_base + cc) * n + row) * W32 + w] = x;
+      if (row < n) out[((size_t)(out_base + cc) * n + row) * W32 + w] = x;
     }
     if (row < n)
-      for (int w = g + 1; w < W32; ++w) out[((size_t)(p.out_base + cc) * n + row) * W32 + w] = 0u;
+      for (int w = g + 1; w < W32; ++w) out[((size_t)(out_base + cc) * n + row) * W32 + w] = 0u;
   }
-  (void)scratch;
+}
+
+// Scratch of one K2 warp: shared-memory views (graph blob, E, spilled A' slots) and TMEM.
+template <typename ET, bool TM>
+struct ScanCtx {
+  const int64_t* M;
+  const int64_t* C;
+  const int4* nrec;
+  const int2* drec;
+  const int32_t* qinfo;
+  ET* E;                      // [32 stages][32 lanes]
+  AView<TM> A;
+  bool all_tm;
+};
+
+template <typename ET, bool TM>
+__device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigned char* smem, int wk, uint32_t tmem_base) {
+  ScanCtx<ET, TM> x;
+  const int lane = threadIdx.x & 31;
+  x.M = reinterpret_cast<const int64_t*>(smem);
+  x.C = x.M + p.n;
+  x.nrec = reinterpret_cast<const int4*>(smem + p.o_nrec);
+  x.drec = reinterpret_cast<const int2*>(smem + p.o_drec);
+  x.qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
+  unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
+  x.E = reinterpret_cast<ET*>(wr);
+  x.A.sm = reinterpret_cast<uint32_t*>(x.E + 32 * 32);                 // [slot][lane] (spill part)
+  x.A.lane = lane;
+  x.A.tmc = TM ? min(p.n_slot, 256) : 0;
+  // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
+  x.A.taddr = TM ? tmem_base + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16) + 256u * (uint32_t)((wk >> 2) & 1) : 0u;
+  x.all_tm = TM && p.n_slot <= 256;
+  return x;
+}
+
+// L2-prefetch the candidate blocks a later task (group gn, candidates cn = first + lane) reads.
+__device__ __forceinline__ void scan_prefetch(const ScanParams& p, const uint32_t* ws, int64_t n_cand, int gn,
+                                              int64_t cn) {
+  const int n = p.n, G = p.G;
+  if (cn >= n_cand) return;
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(ws + cn * p.cs);
+  const unsigned char* col = b + 4 * (size_t)grp_off(gn);
+  if (32 * gn + 1 < n) {                                            // the group has Sn columns
+    for (int off = 0; off < 128 * (gn + 1); off += 128) prefetch_l2(col + off);
+    prefetch_l2(col + 128 * (gn + 1) - 4);                          // the block is 16-byte aligned
+  }
+  prefetch_l2(b + 4 * ((size_t)p.brow + (size_t)gn * G));
+  const unsigned char* ms = b + 4 * (size_t)block_words(G) + 8 * (size_t)(32 * gn);
+  prefetch_l2(ms);
+  prefetch_l2(ms + 128);
+  prefetch_l2(ms + 255);
+}
+
+// One K2 task: stage group g of the 32 candidates batch0 .. batch0+31 of a buffer `ws` holding
+// n_cand candidate blocks; writes part[c][g] = {max_t (mass_t + E_t) over the group's stages,
+// the group's cost} and (optionally) the group's rows of the R / S masks (global candidate
+// index out_base + c).  Everything the task reads from `ws` bypasses L1 (.cg): the fused kernel
+// rewrites a ring slot in the same launch.
+template <typename ET, bool TM>
+__device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET, TM>& x, int g, int64_t batch0,
+                                          uint32_t* ws, int64_t n_cand, int64_t* part, int64_t out_base) {
+  const int lane = threadIdx.x & 31;
+  const int n = p.n, G = p.G;
+  const int64_t* M = x.M;
+  const int64_t* C = x.C;
+  const int4* nrec = x.nrec;
+  const int2* drec = x.drec;
+  const int32_t* qinfo = x.qinfo;
+  ET* E = x.E;
+  const AView<TM>& A = x.A;
+  const bool all_tm = x.all_tm;
+  const int64_t c = batch0 + lane;
+  const bool live = c < n_cand;
+  const int nk = min(n, 32 * (g + 1));                            // nodes 0..nk-1
+  const int nq = (nk + 3) >> 2;                                   // uint4 blocks of Sn
+  uint32_t* cw = ws + (live ? c : 0) * p.cs;
+  const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
+  const bool lsn = live && 32 * g + 1 < n;                        // K1 wrote Sn for this group
+  if (p.s_mask32) emit_mask<true>(p, ws, n_cand, out_base, p.s_mask32, g, nk, batch0, lane);   // before R overwrites
+  // slots: A'_i = Sn_i (Acc_i = 0) for the slotted nodes of the pass.  qinfo[q] = first slot
+  // of quad q | (4-bit mask of its slotted nodes) << 16 (slots ascend with the node index).
+  {  // software-pipelined: the loads of 8 quads are in flight while the previous 8 are stored
+    uint4 va[8], vb[8];
+    int qa[8], qb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      va[u] = (lsn && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
+      qa[u] = u < nq ? qinfo[u] : 0;
+    }
+    for (int q0 = 0; q0 < nq; q0 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vb[u] = (lsn && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
+        qb[u] = q0 + 8 + u < nq ? qinfo[q0 + 8 + u] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i0 = 4 * (q0 + u);
+        if (i0 >= nk) break;                                      // warp-uniform
+        const uint32_t wv[4] = {va[u].x, va[u].y, va[u].z, va[u].w};
+        int s = qa[u] & 0xffff;
+        const int msk = (qa[u] >> 16) & (i0 + 4 <= nk ? 15 : (1 << (nk - i0)) - 1);
+        if (msk == 15 && all_tm) {                                // four consecutive slots
+          A.st4(s, va[u]);
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if ((msk >> j) & 1) {
+            if (!TM) A.template st<0>(s, wv[j]);
+            else if (all_tm) A.template st<2>(s, wv[j]);
+            else A.template st<1>(s, wv[j]);
+            ++s;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        va[u] = vb[u];
+        qa[u] = qb[u];
+      }
+    }
+  }
+  // E_t after stage t's first event, the compute of its own node t (see events())
+  for (int b = 0; b < 32; ++b) E[32 * b + lane] = 32 * g + b < n ? (ET)M[32 * g + b] : (ET)0;
+  __syncwarp();
+  const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
+  int64_t costL = 0;
+  uint32_t* rcol = cw + grp_off(g);
+  if (p.r_mask32) {
+    if (!TM) walk<ET, TM, 0, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    else if (all_tm) walk<ET, TM, 2, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    else walk<ET, TM, 1, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+  } else {
+    if (!TM) walk<ET, TM, 0, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    else if (all_tm) walk<ET, TM, 2, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    else walk<ET, TM, 1, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+  }
+  A.wait_st();                                                    // next task re-fills the slots
+  // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
+  const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
+  int64_t mv[32];
+#pragma unroll
+  for (int b = 0; b < 32; ++b) {                                  // issue all 32 loads first
+    const int r = 32 * g + b;
+    mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
+  }
+  int64_t pk = INT64_MIN;
+#pragma unroll
+  for (int b = 0; b < 32; ++b)
+    if (32 * g + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * b + lane]);
+  if (live) {
+    int64_t* pp = part + 2 * (c * G + g);
+    pp[0] = pk;
+    pp[1] = costL;
+  }
+  if (p.r_mask32) {
+    __syncwarp();
+    __threadfence_block();
+    emit_mask<false>(p, ws, n_cand, out_base, p.r_mask32, g, nk, batch0, lane);
+  }
+  __syncwarp();
 }
 
 // ET = int32_t when every M is a multiple of a scale s with sum M/s < 2^30 (the host checks;
@@ -687,16 +860,7 @@ __device__ void emit_mask(const ScanParams& p, uint32_t* out, int g, int nk, int
 template <typename ET, bool TM>
 __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   // <= 128 regs: co-resides with K1
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = p.n, G = p.G;
-  const int64_t* M = reinterpret_cast<const int64_t*>(smem);
-  const int64_t* C = M + n;
-  const int4* nrec = reinterpret_cast<const int4*>(smem + p.o_nrec);
-  const int2* drec = reinterpret_cast<const int2*>(smem + p.o_drec);
-  const int32_t* qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
-  unsigned char* wr = smem + p.blob_bytes + (size_t)warp * p.warp_bytes;
-  ET* E = reinterpret_cast<ET*>(wr);                               // [32 stages][32 lanes]
-  uint32_t* Asm = reinterpret_cast<uint32_t*>(E + 32 * 32);         // [slot][lane] (spill part)
+  const int warp = threadIdx.x >> 5;
   __shared__ uint32_t tmem_base;
   for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
@@ -708,132 +872,22 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
   if (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  AView<TM> A;
-  A.sm = Asm;
-  A.lane = lane;
-  A.tmc = TM ? min(p.n_slot, 256) : 0;
-  A.taddr = TM ? tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2) : 0u;
-  const bool all_tm = TM && p.n_slot <= 256;
-
+  const ScanCtx<ET, TM> x = scan_ctx<ET, TM>(p, smem, warp, TM ? tmem_base : 0u);
+  const int G = p.G;
+  const int lane = threadIdx.x & 31;
   const int tasks = G * p.n_batch;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   for (int task = gw; task < tasks; task += nwarps) {
     const int g = G - 1 - task / p.n_batch;                         // big groups first
     const int64_t batch0 = (int64_t)(task % p.n_batch) * 32;
-    const int64_t c = batch0 + lane;
-    const bool live = c < p.n_cand;
-    const int nk = min(n, 32 * (g + 1));                            // nodes 0..nk-1
-    const int nq = (nk + 3) >> 2;                                   // uint4 blocks of Sn
-    uint32_t* cw = p.ws + (live ? c : 0) * p.cs;
-    const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
-    const bool lsn = live && 32 * g + 1 < n;                        // K1 wrote Sn for this group
-    {  // pull the warp's next task (Sn columns, row-32g words, masses) towards L2 meanwhile
-      const int tn = task + nwarps;
-      if (p.prefetch && tn < tasks) {
-        const int gn = G - 1 - tn / p.n_batch;
-        const int64_t cn = (int64_t)(tn % p.n_batch) * 32 + lane;
-        if (cn < p.n_cand) {
-          const unsigned char* b = reinterpret_cast<const unsigned char*>(p.ws + cn * p.cs);
-          const unsigned char* col = b + 4 * (size_t)grp_off(gn);
-          if (32 * gn + 1 < n) {                                    // the group has Sn columns
-            for (int off = 0; off < 128 * (gn + 1); off += 128) prefetch_l2(col + off);
-            prefetch_l2(col + 128 * (gn + 1) - 4);                  // the block is 16-byte aligned
-          }
-          prefetch_l2(b + 4 * ((size_t)p.brow + (size_t)gn * G));
-          const unsigned char* ms = b + 4 * (size_t)block_words(G) + 8 * (size_t)(32 * gn);
-          prefetch_l2(ms);
-          prefetch_l2(ms + 128);
-          prefetch_l2(ms + 255);
-        }
-      }
-    }
-    if (p.s_mask32) emit_mask<true>(p, p.s_mask32, g, nk, batch0, lane, nullptr);   // before R overwrites
-    // slots: A'_i = Sn_i (Acc_i = 0) for the slotted nodes of the pass.  qinfo[q] = first slot
-    // of quad q | (4-bit mask of its slotted nodes) << 16 (slots ascend with the node index).
-    {  // software-pipelined: the loads of 8 quads are in flight while the previous 8 are stored
-      uint4 va[8], vb[8];
-      int qa[8], qb[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        va[u] = (lsn && u < nq) ? __ldcg(sn4 + u) : make_uint4(0u, 0u, 0u, 0u);
-        qa[u] = u < nq ? qinfo[u] : 0;
-      }
-      for (int q0 = 0; q0 < nq; q0 += 8) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          vb[u] = (lsn && q0 + 8 + u < nq) ? __ldcg(sn4 + q0 + 8 + u) : make_uint4(0u, 0u, 0u, 0u);
-          qb[u] = q0 + 8 + u < nq ? qinfo[q0 + 8 + u] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i0 = 4 * (q0 + u);
-          if (i0 >= nk) break;                                      // warp-uniform
-          const uint32_t wv[4] = {va[u].x, va[u].y, va[u].z, va[u].w};
-          int s = qa[u] & 0xffff;
-          const int msk = (qa[u] >> 16) & (i0 + 4 <= nk ? 15 : (1 << (nk - i0)) - 1);
-          if (msk == 15 && all_tm) {                                // four consecutive slots
-            A.st4(s, va[u]);
-            continue;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if ((msk >> j) & 1) {
-              if (!TM) A.template st<0>(s, wv[j]);
-              else if (all_tm) A.template st<2>(s, wv[j]);
-              else A.template st<1>(s, wv[j]);
-              ++s;
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          va[u] = vb[u];
-          qa[u] = qb[u];
-        }
-      }
-    }
-    for (int b = 0; b < 32; ++b) E[32 * b + lane] = (ET)0;
-    __syncwarp();
-    const uint32_t* brow = cw + p.brow + g * G;                     // S row 32g, row form
-    int64_t costL = 0;
-    uint32_t* rcol = cw + grp_off(g);
-    if (p.r_mask32) {
-      if (!TM) walk<ET, TM, 0, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else if (all_tm) walk<ET, TM, 2, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else walk<ET, TM, 1, true>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    } else {
-      if (!TM) walk<ET, TM, 0, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else if (all_tm) walk<ET, TM, 2, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-      else walk<ET, TM, 1, false>(nq - 1, nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    }
-    A.wait_st();                                                    // next task re-fills the slots
-    // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
-    const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
-    int64_t mv[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) {                                  // issue all 32 loads first
-      const int r = 32 * g + b;
-      mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
-    }
-    int64_t pk = INT64_MIN;
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      if (32 * g + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * b + lane]);
-    if (live) {
-      int64_t* pp = p.part + 2 * (c * G + g);
-      pp[0] = pk;
-      pp[1] = costL;
-    }
-    if (p.r_mask32) {
-      __syncwarp();
-      __threadfence_block();
-      emit_mask<false>(p, p.r_mask32, g, nk, batch0, lane, nullptr);
-    }
-    __syncwarp();
+    const int tn = task + nwarps;                                   // pull the next task towards L2
+    if (p.prefetch && tn < tasks)
+      scan_prefetch(p, p.ws, p.n_cand, G - 1 - tn / p.n_batch, (int64_t)(tn % p.n_batch) * 32 + lane);
+    scan_task<ET, TM>(p, x, g, batch0, p.ws, p.n_cand, p.part, p.out_base);
   }
   if (TM) {
-    A.wait_st();
+    x.A.wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -855,17 +909,16 @@ struct ReduceParams {
   int64_t* best_key;
 };
 
-__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= p.n_cand) return;
-  const int64_t* pp = p.part + 2 * c * p.G;
+// peak / cost / a7 keys of candidate c (part rows c, output index out_base + c).
+__device__ __forceinline__ void reduce_one(const ReduceParams& p, const int64_t* part, int64_t c, int64_t out_base) {
+  const int64_t* pp = part + 2 * c * p.G;
   int64_t pk = INT64_MIN, cs = 0;
   for (int g = 0; g < p.G; ++g) {
     pk = max(pk, __ldcg(pp + 2 * g));
     cs += __ldcg(pp + 2 * g + 1);
   }
   pk = p.ovh + p.mscale * pk;
-  const int64_t local = p.out_base + c;
+  const int64_t local = out_base + c;
   p.peak[local] = pk;
   p.cost[local] = cs;
   const int64_t key = (cs << p.idx_bits) | (p.index_base + local);
@@ -875,6 +928,167 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
       if (key < cur) atomicMin(reinterpret_cast<long long*>(p.best_key + b), (long long)key);
     }
   }
+}
+
+template <int = 0>
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= p.n_cand) return;
+  reduce_one(p, p.part, c, p.out_base);
+}
+
+// ------------------------------------------------------------------------------------ fused
+// One persistent launch per call (n_theta <= 4, int32 scan state, A' in TMEM): every CTA runs
+// KF1 = k1_warps(NT) rounding warps (the K1 body) and KF2 = 8 scan warps (the K2 task body)
+// side by side, handing the stage-sliced S columns over through a ring of R slots in global
+// memory that stays L2-resident (a slot = one unit of 32 S*: 32 n_theta candidate blocks plus
+// their per-group partials, ~0.43 MB at n = 353).  Unit u lives in slot u % R.
+//   K1 warp, S* s of unit u = s / 32:  wait freed[slot] >= u / R  (the slot's previous unit is
+//     scanned and reduced), write the blocks, then fence + filled[slot] += 1.
+//   K2 warp: take task tickets in order (one atomic per task: dynamic balance over tasks of very
+//     different length); task (u, g, batch) waits filled[slot] >= 32 (u / R) + |u|, runs the scan
+//     task, fences, done[slot] += 1; the warp that completes unit u reduces its candidates
+//     (peak, cost, per-budget keys: the K3 step) right there, then freed[slot] += 1.
+// Deadlock-free: the smallest unwritten S* belongs to a unit whose slot predecessor is complete
+// (all its S* are smaller), and tickets are issued in unit order, so that predecessor's tasks
+// are held by warps that can run them.  One launch removes the two-kernel pipeline's fill and
+// drain, its per-chunk prologues and tails, and the DRAM round trip of the chunk buffers.
+struct FusedParams {
+  RoundParams rp;             // rp.s_begin = 0, rp.s_count = n_sstar, rp.th0 = 0, rp.nt = n_theta
+  ScanParams sp;              // per-task buffer fields unused
+  ReduceParams qp;            // part / n_cand / out_base unused
+  uint32_t* ring;             // n_slots slots of slot_words words
+  int64_t slot_words;         // 32 n_theta cs words of candidate blocks, then the partials
+  int32_t n_slots;
+  uint32_t* ctl;              // [0] task ticket, [1 + slot] filled, [1 + R + slot] done,
+                              // [1 + 2R + slot] freed, [1 + 3R] S* ticket (zeroed per call)
+  int32_t n_sstar, n_theta;
+  int32_t n_units;
+  int32_t tpu;                // tasks of a full unit: G * n_theta
+  int64_t total_tasks;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// lane 0 waits until *p >= target (then the warp proceeds); exponential back-off sleep
+__device__ __forceinline__ void warp_wait_geq(const uint32_t* p, uint32_t target) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t ns = 32;
+    while (ld_acquire(p) < target) {
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : ns;
+    }
+  }
+  __syncwarp();
+}
+
+struct K1Ring {
+  uint32_t* ring;
+  int64_t slot_words;
+  int32_t n_slots, n_theta, cs;
+  uint32_t* ctl;
+  // S* tickets (in order across all K1 warps; a CTA that starts late simply takes later ones)
+  __device__ __forceinline__ int first() const {
+    uint32_t t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(ctl + 1 + 3 * n_slots, 1u);
+    return (int)__shfl_sync(FULL, t, 0);
+  }
+  __device__ __forceinline__ int next(int) const { return first(); }
+  __device__ __forceinline__ uint32_t* begin(int s) const {
+    const int u = s >> 5, slot = u % n_slots, k = u / n_slots;
+    if (k > 0) warp_wait_geq(ctl + 1 + 2 * n_slots + slot, (uint32_t)k);
+    return ring + (int64_t)slot * slot_words + (int64_t)(s & 31) * n_theta * cs;
+  }
+  __device__ __forceinline__ void end(int s) const {
+    __threadfence();                                                // this lane's blocks, then the count
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) atomicAdd(ctl + 1 + (s >> 5) % n_slots, 1u);
+  }
+};
+
+constexpr int kFusedScanWarps = 8;
+__host__ __device__ constexpr int fused_warps(int nt) { return k1_warps(nt) + kFusedScanWarps; }
+// dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
+__host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, bool bulk) {
+  return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1023) & ~(size_t)1023;
+}
+
+template <int NT, bool BULK>
+__global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
+                                                                         const __grid_constant__ CUtensorMap tmap) {
+  using ET = int32_t;
+  constexpr int KF1 = k1_warps(NT);
+  extern __shared__ __align__(1024) unsigned char fraw[];
+  unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
+  unsigned char* k1smem = base;
+  unsigned char* k2smem = base + fused_k1_bytes(NT, fp.rp.nib32 ? fp.rp.nib_entries : 0, BULK);
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ScanParams& sp = fp.sp;
+  k1_setup<NT, BULK>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
+  for (int i = threadIdx.x; i < sp.blob_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(k2smem)[i] = sp.blob[i];
+  if (warp == KF1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_base)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (warp < KF1) {                                                 // ---- rounding (K1) warps
+    __shared__ int sq[KF1][8];
+    const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl};
+    k1_body<NT, BULK>(fp.rp, &tmap, k1smem, warp, sq[warp], hk);
+    return;
+  }
+  // ---- scan (K2) warps
+  const int wk = warp - KF1;
+  const ScanCtx<ET, true> x = scan_ctx<ET, true>(sp, k2smem, wk, tmem_base);
+  const int G = sp.G;
+  const int R = fp.n_slots;
+  const int64_t unit_cands = 32 * (int64_t)fp.n_theta;
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(fp.ctl, 1u);
+    t = __shfl_sync(FULL, t, 0);
+    if ((int64_t)t >= fp.total_tasks) break;
+    const int u = (int)(t / (uint32_t)fp.tpu);
+    const int sub = (int)(t - (uint32_t)u * (uint32_t)fp.tpu);
+    const int ns = min(32, fp.n_sstar - 32 * u);                   // S* of this unit
+    const int64_t ncand = (int64_t)ns * fp.n_theta;
+    const int nb = (int)((ncand + 31) / 32);                        // candidate batches of the unit
+    const int g = G - 1 - sub / nb;                                 // big groups first
+    const int batch = sub % nb;
+    const int slot = u % R, k = u / R;
+    uint32_t* ws = fp.ring + (int64_t)slot * fp.slot_words;
+    int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
+    warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
+    scan_task<ET, true>(sp, x, g, (int64_t)batch * 32, ws, ncand, part, (int64_t)u * unit_cands);
+    __threadfence();                                                // reads done, partials visible
+    __syncwarp();
+    const uint32_t tasks_u = (uint32_t)(G * nb);
+    uint32_t old = 0;
+    if (lane == 0) old = atomicAdd(fp.ctl + 1 + R + slot, 1u);
+    old = __shfl_sync(FULL, old, 0);
+    if (old + 1 == (uint32_t)fp.tpu * (uint32_t)k + tasks_u) {       // last task of unit u: reduce it
+      __threadfence();
+      for (int64_t c = lane; c < ncand; c += 32) reduce_one(fp.qp, part, c, (int64_t)u * unit_cands);
+      __threadfence();                                              // partials read: release the slot
+      __syncwarp();
+      if (lane == 0) atomicAdd(fp.ctl + 1 + 2 * R + slot, 1u);
+    }
+  }
+  x.A.wait_st();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("bar.sync 1, %0;" :: "r"(32 * kFusedScanWarps) : "memory");   // the scan warps only
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == KF1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem_base) : "memory");
 }
 
 }  // namespace cm2

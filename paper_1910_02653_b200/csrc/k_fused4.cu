@@ -1,0 +1,3 @@
+// Instances: fused persistent kernels, 4 threshold(s) per pass (see cm_inst.cuh).
+#include "cm_inst.cuh"
+CM_FUSED(4, false) CM_FUSED(4, true)

@@ -11,6 +11,8 @@ from workloads.sstar import dense_to_tri4, from_binary, gen_sstar, roundup4
 pytestmark = pytest.mark.gpu
 
 KEY_NONE = (1 << 63) - 1
+# dense: K1 reads 32x32 blocks by tensor-map TMA; tri4: by per-row 1-D bulk copies
+LAYOUTS = ["dense", "tri4"]
 
 
 def gpu_run(g, sstar, thetas, budgets=None, layout="dense", masks=False, index_base=0,
@@ -65,37 +67,42 @@ def compare(g, sstar_dense, thetas, budgets=None, masks=False, layout="dense", i
     return res, outs
 
 
-def test_config1_path8():
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_config1_path8(layout):
     """BASELINE config 1: path n=8, unit C/M, 64 S* x 4 thresholds x 3 budgets."""
     g = G.path(8)
     x = gen_sstar(g, "mix", 1, 0, 64)
-    compare(g, x, [0.3, 0.4, 0.5, 0.6], [2, 4, 8], masks=True)
+    compare(g, x, [0.3, 0.4, 0.5, 0.6], [2, 4, 8], masks=True, layout=layout)
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13])
 @pytest.mark.parametrize("fam", ["g1", "g2"])
-def test_small_random(n, fam):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_small_random(n, fam, layout):
     g = G.random_dag(n, 0.4, 10 + n)
     x = gen_sstar(g, fam, 3, 0, 8)
-    compare(g, x, [0.5, 0.2], [g.ovh + 5, g.ovh + 20, 10 ** 9], masks=True)
+    compare(g, x, [0.5, 0.2], [g.ovh + 5, g.ovh + 20, 10 ** 9], masks=True, layout=layout)
 
 
 @pytest.mark.parametrize("n", [31, 32, 33, 63, 64, 65, 95, 96, 97, 127, 128, 129, 191, 257])
-def test_word_boundaries(n):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_word_boundaries(n, layout):
     g = G.random_dag(n, 0.05, n)
     x = gen_sstar(g, "g1" if n % 2 else "g2", 5, 0, 3)
-    compare(g, x, [0.5, 0.8], [B.p_floor(g), B.p_live(g)], masks=True)
+    compare(g, x, [0.5, 0.8], [B.p_floor(g), B.p_live(g)], masks=True, layout=layout)
 
 
 @pytest.mark.parametrize("L", [15, 16, 17, 31, 32, 33, 48])
-def test_training_random(L):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_training_random(L, layout):
     g = G.random_training(L, 0.05, L)
     x = gen_sstar(g, "mix", 7, 0, 4)
-    compare(g, x, [0.5], B.geometric_grid(g, 5), masks=True)
+    compare(g, x, [0.5], B.geometric_grid(g, 5), masks=True, layout=layout)
 
 
 @pytest.mark.parametrize("name", ["vgg16", "resnet50", "unet", "mobilenet", "fcn8"])
-def test_paper_shaped(name):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_paper_shaped(name, layout):
     g = G.NETWORKS[name]()
     if name == "unet":
         base = g
@@ -104,7 +111,7 @@ def test_paper_shaped(name):
     else:
         budgets = B.geometric_grid(g, 16)
     x = gen_sstar(g, "mix", 11, 100, 3)
-    compare(g, x, [0.5, 0.35], budgets, masks=(name == "resnet50"))
+    compare(g, x, [0.5, 0.35], budgets, masks=(name == "resnet50"), layout=layout)
 
 
 def test_layouts_and_ld():
@@ -116,7 +123,8 @@ def test_layouts_and_ld():
     assert np.array_equal(r1["peak"], r2["peak"]) and np.array_equal(r1["cost"], r2["cost"])
 
 
-def test_rounding_edge_values():
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_rounding_edge_values(layout):
     """Exact 0.5 ties, NaN, theta 0 and 1, garbage in the never-read upper triangle."""
     g = G.random_training(10, 0.2, 4)
     x = gen_sstar(g, "g2", 9, 0, 4, upper=np.nan)
@@ -124,7 +132,7 @@ def test_rounding_edge_values():
     x[1][3, 1] = np.nan
     x[1][7, 2:5] = np.nan
     x[2] = np.where(np.tril(np.ones_like(x[2], bool), -1), np.float32(1.0), np.float32(7.0))
-    compare(g, x, [0.5, 0.0, 1.0, np.nextafter(np.float32(0.5), np.float32(0))], masks=True)
+    compare(g, x, [0.5, 0.0, 1.0, np.nextafter(np.float32(0.5), np.float32(0))], masks=True, layout=layout)
 
 
 def test_binary_patterns_closed_forms():
@@ -177,11 +185,12 @@ def test_error_paths_on_device():
         cm.round_and_evaluate(gb, xb, th, total_candidates=1 << 20)
 
 
-def test_max_n():
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_max_n(layout):
     """n = CM_NMAX = 1024 (32 words per row, 1024 threads)."""
     g = G.random_dag(1024, 0.0015, 77)
     x = gen_sstar(g, "g1", 3, 0, 2)
-    compare(g, x, [0.5], [B.p_live(g)])
+    compare(g, x, [0.5], [B.p_live(g)], layout=layout)
 
 
 def test_device_generator_matches_host():
@@ -239,12 +248,13 @@ def test_full_size_sampled():
 
 
 @pytest.mark.parametrize("seed", [1, 2])
-def test_int64_state_path(seed):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_int64_state_path(seed, layout):
     """M values too large for the int32 scan state (sum M / gcd >= 2^30): int64 kernels."""
     g = G.random_training(20, 0.1, seed)
     g.mem = g.mem * (1 << 35) + np.arange(g.n, dtype=np.int64) * 7 + 3    # gcd 1, huge sums
     x = gen_sstar(g, "mix", 4, 0, 6)
-    compare(g, x, [0.5, 0.7], [B.p_floor(g), B.p_live(g)], masks=True)
+    compare(g, x, [0.5, 0.7], [B.p_floor(g), B.p_live(g)], masks=True, layout=layout)
 
 
 def test_scaled_int32_path():
@@ -253,3 +263,11 @@ def test_scaled_int32_path():
     g.mem = g.mem * 1000                                   # sum M >> 2^31, sum M / gcd small
     x = gen_sstar(g, "g1", 8, 0, 3)
     compare(g, x, [0.5], B.geometric_grid(g, 8))
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_many_thresholds(layout):
+    """Six thresholds: two K1 passes per S* (4 + 2 thresholds)."""
+    g = G.random_training(24, 0.1, 5)
+    x = gen_sstar(g, "mix", 12, 0, 5)
+    compare(g, x, [0.5, 0.1, 0.9, 0.3, 0.7, 0.45], B.geometric_grid(g, 4), masks=True, layout=layout)
