@@ -271,3 +271,70 @@ def test_many_thresholds(layout):
     g = G.random_training(24, 0.1, 5)
     x = gen_sstar(g, "mix", 12, 0, 5)
     compare(g, x, [0.5, 0.1, 0.9, 0.3, 0.7, 0.45], B.geometric_grid(g, 4), masks=True, layout=layout)
+
+
+@pytest.fixture
+def env_var():
+    """Set library tuning variables for one test (read by the library at every call)."""
+    import os
+    saved = {}
+
+    def setter(**kv):
+        for k, v in kv.items():
+            saved.setdefault(k, os.environ.get(k))
+            os.environ[k] = str(v)
+    yield setter
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_fused_ring_wraparound(env_var, layout):
+    """Fused path with a 3-slot ring: 1000 S* = 32 units, every slot reused ~10 times
+    (producer / consumer hand-off, slot release after the in-kernel reduce)."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    env_var(CM_RING=3)
+    g = G.resnet50()
+    N = 1000
+    dg = DeviceGenerator(g, "g1", 77, layout=layout)
+    buf = torch.empty(dg.shape(N), dtype=torch.float32, device="cuda")
+    dg.fill(buf, 0)
+    graph = cm.Graph.from_workload(g)
+    budgets = B.geometric_grid(g, 6)
+    th = torch.tensor([0.5, 0.3], device="cuda")
+    out = cm.round_and_evaluate(graph, buf, th, torch.tensor(budgets, device="cuda"), layout=layout)
+    torch.cuda.synchronize()
+    assert cm.debug_last_launches() == 1                           # the fused kernel ran
+    peak, cost = out["peak"].cpu().numpy(), out["cost"].cpu().numpy()
+    inst = Instance.from_graph(g)
+    for s in [0, 31, 32, 500, 777, N - 1]:
+        x = gen_sstar(g, "g1", 77, s, 1)[0]
+        for j, t in enumerate([0.5, 0.3]):
+            o = evaluate(inst, x, t)
+            assert (peak[2 * s + j], cost[2 * s + j]) == (o["peak"], o["cost"]), (s, j)
+    bits = out["idx_bits"]
+    for b, key in enumerate(out["best_key"].cpu().numpy()):
+        feas = np.nonzero(peak <= budgets[b])[0]
+        if len(feas) == 0:
+            assert key == KEY_NONE
+            continue
+        c = cost[feas].min()
+        assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, feas[cost[feas] == c].min())
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("name", ["vgg16", "resnet50", "fcn8"])
+def test_two_kernel_pipeline(env_var, name, layout):
+    """The two-kernel chunked pipeline (used for > 4 thresholds, the int64 state, or without
+    TMEM) forced on the paper-shaped graphs, with a workspace small enough for several chunks."""
+    import paper_1910_02653_b200 as cm
+    env_var(CM_FUSED=0, CM_WS_MB=1)                                 # minimum workspace: 1024 candidates
+    g = G.NETWORKS[name]()
+    x = gen_sstar(g, "mix", 13, 40, 700 if name == "vgg16" else 70)   # vgg16: 2 chunks
+    compare(g, x, [0.5, 0.25], B.geometric_grid(g, 8), layout=layout)
+    assert cm.debug_last_launches() >= 3
