@@ -89,8 +89,8 @@ EncodeTiledFn encode_tiled() {
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
-size_t scan_warp_bytes(int n_slot, bool s32, bool tm) {
-  const int spill = std::max(0, n_slot - (tm ? 256 : 0));          // A' slots kept in shared memory
+size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
+  const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
   return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * spill;
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
@@ -288,12 +288,13 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   if (g->scan32 && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
     const int nt = a->n_theta;
     const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
-    const size_t smemf = k1b + fixed + wb * cm2::kFusedScanWarps + 1024;
+    const size_t wbf = scan_warp_bytes(g->n_slot, true, true, cm2::kFusedTmemCols);
+    const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
     const int64_t total_tasks = (units - 1) * (int64_t)G * nt +
                                 (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
-    int64_t ring_max = env_flag("CM_RING", 512);   // measured: 64 -> 5.8, 256 -> 14.4, 512+ -> 14.8 M cand/s
+    int64_t ring_max = env_flag("CM_RING", 768);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
     int64_t R = std::min<int64_t>(ring_max, units);
     auto ctl_bytes = [](int64_t r) { return (4 * (2 + 3 * r) + 255) & ~int64_t(255); };
     while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
@@ -330,6 +331,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         rp.sn = nullptr;
         fp.rp = rp;
         fp.sp = sp;
+        fp.sp.warp_bytes = (int32_t)wbf;
         fp.qp = qp;
         uint32_t* ctl = reinterpret_cast<uint32_t*>(ws);
         fp.ctl = ctl;
@@ -623,17 +625,20 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     for (int32_t j : users[i])
       if (j != i + 1) { slot[i] = g->n_slot++; break; }
   size_t base2 = (16 * (size_t)n + 4 * (size_t)(n + 1 + E) + 15) & ~size_t(15);
-  g->o_nrec = (int32_t)base2;
-  g->o_drec = (int32_t)(base2 + 16 * (size_t)n);
-  g->o_qinfo = (int32_t)(base2 + 16 * (size_t)n + 8 * (size_t)E);
+  // node records start one record in: record -1 is a sentinel {0, 0, 0, -1} (no slot), so the
+  // walk reads the record of node k-1 without a k > 0 test
+  g->o_nrec = (int32_t)(base2 + 16);
+  g->o_drec = (int32_t)(base2 + 16 * (size_t)(n + 1));
+  g->o_qinfo = (int32_t)(base2 + 16 * (size_t)(n + 1) + 8 * (size_t)E);
   const int nquad = (n + 3) / 4;
-  size_t bytes2 = (base2 + 16 * (size_t)n + 8 * (size_t)E + 4 * (size_t)nquad + 15) & ~size_t(15);
+  size_t bytes2 = (base2 + 16 * (size_t)(n + 1) + 8 * (size_t)E + 4 * (size_t)nquad + 15) & ~size_t(15);
   g->blob2_bytes = (int32_t)bytes2;
   std::vector<unsigned char> blob2(bytes2, 0);
   std::memcpy(blob2.data(), blob.data(), 16 * (size_t)n + 4 * (size_t)(n + 1 + E));
   for (int i = 0; i < n; ++i) reinterpret_cast<int64_t*>(blob2.data())[i] = mem[i] / g->mscale;
   {
     int32_t* nr = reinterpret_cast<int32_t*>(blob2.data() + g->o_nrec);
+    nr[-1] = -1;                                        // sentinel record -1: {0, 0, 0, -1}
     int32_t* dr = reinterpret_cast<int32_t*>(blob2.data() + g->o_drec);
     int32_t ef = 0;
     for (int k = 0; k < n; ++k) {

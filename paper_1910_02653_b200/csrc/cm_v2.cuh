@@ -308,7 +308,11 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
       if (pol)
         tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
       else
+#ifdef CM_EXP_L2INPUT
+        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)((p.s_begin + ps) & 63), &bars[pstage]);   // timing experiment
+#else
         tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
+#endif
     }
     pstage = pstage + 1 == kSt ? 0 : pstage + 1;
     if (++pw > pg) {
@@ -555,6 +559,20 @@ __device__ __forceinline__ void node_step(uint32_t Rk, uint32_t diag, uint32_t s
     events<1, ET>(Rk & ~diag, sf, Mk, &fa, &ma, E, lane);
     return;
   }
+  if (ndf == 1) {                                                   // the common far case
+    const int2 d = drec[e0];
+    const int s0 = d.x & 0xffff;
+    uint32_t f[2] = {0u, fa};
+    ET m[2] = {sizeof(ET) == 4 ? (ET)d.y : (ET)M[d.x >> 16], ma};
+    if (st_pending) A.wait_st();
+    uint32_t a0 = A.template ld_async<MODE>(s0);
+    A.wait_ld(a0);
+    f[0] = Rk & ~a0;                                                // FREE_{t,i,k} = R_k & ~A'_i
+    A.template st<MODE>(s0, a0 | Rk);                               // A'_i |= R_k
+    st_pending = true;
+    events<2, ET>(Rk & ~diag, sf, Mk, f, m, E, lane);
+    return;
+  }
   uint32_t f[4] = {0u, 0u, 0u, fa};
   ET m[4] = {(ET)0, (ET)0, (ET)0, ma};
   int sl[3] = {0, 0, 0};
@@ -608,6 +626,8 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
   uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
   uint32_t bnext = (g > 0 && (k0 >> 5) >= 1 && live) ? __ldcg(brow + (k0 >> 5) - 1) : 0u;
   int4 rec1 = nrec[k0];                                             // record of the next node
+  // Sn_k: the previous step's Sn_{k-1}, so each step extracts one word of the quads
+  uint32_t sn1 = (k0 & 3) == 3 ? quad.w : (k0 & 3) == 2 ? quad.z : (k0 & 3) == 1 ? quad.y : quad.x;
   uint32_t acc = 0u;                                                // Acc_k from user k+1
   uint32_t bslot = 0u;                                              // A'_k base when k has a slot
   bool st_pending = true;                                           // init stores precede
@@ -621,10 +641,10 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
   for (int k = k0; k >= 0; --k) {
     const int u = k & 3;
     const int4 rec = rec1;
-    rec1 = k > 0 ? nrec[k - 1] : make_int4(0, 0, 0, -1);
+    rec1 = nrec[k - 1];                                             // k = 0: the sentinel record
     const int64_t Ck = C[k];
-    const uint32_t sn = u == 3 ? quad.w : u == 2 ? quad.z : u == 1 ? quad.y : quad.x;
-    const uint32_t sn1 = u == 3 ? quad.z : u == 2 ? quad.y : u == 1 ? quad.x : nquad.w;   // Sn_{k-1}
+    const uint32_t sn = sn1;
+    sn1 = u == 0 ? nquad.w : u == 1 ? quad.x : u == 2 ? quad.y : quad.z;   // Sn_{k-1}
     const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;             // A'_k, complete
     const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);     // S_t from S_{t+1} and row 32g
     const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
@@ -704,8 +724,10 @@ struct ScanCtx {
   bool all_tm;
 };
 
+// tcols: TMEM columns per warp (512 / warps per lane quarter); slots beyond spill to shared memory.
 template <typename ET, bool TM>
-__device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigned char* smem, int wk, uint32_t tmem_base) {
+__device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigned char* smem, int wk, uint32_t tmem_base,
+                                                    int tcols) {
   ScanCtx<ET, TM> x;
   const int lane = threadIdx.x & 31;
   x.M = reinterpret_cast<const int64_t*>(smem);
@@ -717,10 +739,10 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   x.E = reinterpret_cast<ET*>(wr);
   x.A.sm = reinterpret_cast<uint32_t*>(x.E + 32 * 32);                 // [slot][lane] (spill part)
   x.A.lane = lane;
-  x.A.tmc = TM ? min(p.n_slot, 256) : 0;
+  x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
   // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
-  x.A.taddr = TM ? tmem_base + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16) + 256u * (uint32_t)((wk >> 2) & 1) : 0u;
-  x.all_tm = TM && p.n_slot <= 256;
+  x.A.taddr = TM ? tmem_base + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16) + (uint32_t)(tcols * (wk >> 2)) : 0u;
+  x.all_tm = TM && p.n_slot <= tcols;
   return x;
 }
 
@@ -830,16 +852,19 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   A.wait_st();                                                    // next task re-fills the slots
   // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
   const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
-  int64_t mv[32];
-#pragma unroll
-  for (int b = 0; b < 32; ++b) {                                  // issue all 32 loads first
-    const int r = 32 * g + b;
-    mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
-  }
   int64_t pk = INT64_MIN;
 #pragma unroll
-  for (int b = 0; b < 32; ++b)
-    if (32 * g + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * b + lane]);
+  for (int b0 = 0; b0 < 32; b0 += 8) {                              // 8 loads in flight at a time
+    int64_t mv[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int r = 32 * g + b0 + b;
+      mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (32 * g + b0 + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * (b0 + b) + lane]);
+  }
   if (live) {
     int64_t* pp = part + 2 * (c * G + g);
     pp[0] = pk;
@@ -872,7 +897,7 @@ __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   //
   if (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const ScanCtx<ET, TM> x = scan_ctx<ET, TM>(p, smem, warp, TM ? tmem_base : 0u);
+  const ScanCtx<ET, TM> x = scan_ctx<ET, TM>(p, smem, warp, TM ? tmem_base : 0u, 256);
   const int G = p.G;
   const int lane = threadIdx.x & 31;
   const int tasks = G * p.n_batch;
@@ -1009,7 +1034,11 @@ struct K1Ring {
   }
 };
 
-constexpr int kFusedScanWarps = 8;
+#ifndef CM_KF2
+#define CM_KF2 8
+#endif
+constexpr int kFusedScanWarps = CM_KF2;                            // scan warps per fused CTA
+constexpr int kFusedTmemCols = 512 / ((kFusedScanWarps + 3) / 4);  // per scan warp
 __host__ __device__ constexpr int fused_warps(int nt) { return k1_warps(nt) + kFusedScanWarps; }
 // dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
 __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, bool bulk) {
@@ -1048,27 +1077,55 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   }
   // ---- scan (K2) warps
   const int wk = warp - KF1;
-  const ScanCtx<ET, true> x = scan_ctx<ET, true>(sp, k2smem, wk, tmem_base);
+  const ScanCtx<ET, true> x = scan_ctx<ET, true>(sp, k2smem, wk, tmem_base, kFusedTmemCols);
   const int G = sp.G;
   const int R = fp.n_slots;
   const int64_t unit_cands = 32 * (int64_t)fp.n_theta;
-  for (;;) {
+  // tickets are claimed one task ahead, so the next task's blocks can be pulled into L2 while
+  // the current one scans (when its unit is already filled)
+  auto claim = [&]() {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(fp.ctl, 1u);
-    t = __shfl_sync(FULL, t, 0);
-    if ((int64_t)t >= fp.total_tasks) break;
-    const int u = (int)(t / (uint32_t)fp.tpu);
-    const int sub = (int)(t - (uint32_t)u * (uint32_t)fp.tpu);
-    const int ns = min(32, fp.n_sstar - 32 * u);                   // S* of this unit
-    const int64_t ncand = (int64_t)ns * fp.n_theta;
-    const int nb = (int)((ncand + 31) / 32);                        // candidate batches of the unit
-    const int g = G - 1 - sub / nb;                                 // big groups first
-    const int batch = sub % nb;
-    const int slot = u % R, k = u / R;
+    return __shfl_sync(FULL, t, 0);
+  };
+  struct Task {
+    int u, g, batch, slot, k, ns;
+    int64_t ncand;
+  };
+  auto decode = [&](uint32_t t) {
+    Task d;
+    d.u = (int)(t / (uint32_t)fp.tpu);
+    const int sub = (int)(t - (uint32_t)d.u * (uint32_t)fp.tpu);
+    d.ns = min(32, fp.n_sstar - 32 * d.u);                          // S* of this unit
+    d.ncand = (int64_t)d.ns * fp.n_theta;
+    const int nb = (int)((d.ncand + 31) / 32);                      // candidate batches of the unit
+    d.g = G - 1 - sub / nb;                                         // big groups first
+    d.batch = sub % nb;
+    d.slot = d.u % R;
+    d.k = d.u / R;
+    return d;
+  };
+  uint32_t t = claim();
+  while ((int64_t)t < fp.total_tasks) {
+    const uint32_t t_next = claim();
+    const Task d = decode(t);
+    const int u = d.u, g = d.g, batch = d.batch, slot = d.slot, k = d.k, ns = d.ns;
+    const int64_t ncand = d.ncand;
+    const int nb = (int)((ncand + 31) / 32);
     uint32_t* ws = fp.ring + (int64_t)slot * fp.slot_words;
     int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
     warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
+    scan_prefetch(sp, ws, ncand, g, (int64_t)batch * 32 + lane);
+    if ((int64_t)t_next < fp.total_tasks) {
+      const Task e = decode(t_next);
+      bool ready = false;
+      if (lane == 0) ready = ld_acquire(fp.ctl + 1 + e.slot) >= (uint32_t)(32 * e.k + e.ns);
+      if (__shfl_sync(FULL, ready, 0))
+        scan_prefetch(sp, fp.ring + (int64_t)e.slot * fp.slot_words, e.ncand, e.g, (int64_t)e.batch * 32 + lane);
+    }
+#ifndef CM_EXP_NOSCAN
     scan_task<ET, true>(sp, x, g, (int64_t)batch * 32, ws, ncand, part, (int64_t)u * unit_cands);
+#endif
     __threadfence();                                                // reads done, partials visible
     __syncwarp();
     const uint32_t tasks_u = (uint32_t)(G * nb);
@@ -1082,6 +1139,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
       __syncwarp();
       if (lane == 0) atomicAdd(fp.ctl + 1 + 2 * R + slot, 1u);
     }
+    t = t_next;
   }
   x.A.wait_st();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
