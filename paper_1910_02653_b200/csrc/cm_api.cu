@@ -131,14 +131,18 @@ int env_flag(const char* name, int dflt) {
 // the never-read upper triangle), yet it measured fastest once rows are 128-byte aligned
 // (ld % 32 == 0): 12.97 vs 12.63 M cand/s (128 B) at n = 353 in the two-kernel pipeline.
 // CM_L2PROMO = 0 / 64 / 128 / 256 (tuning), default 256 (measured best with 128-byte aligned rows).
-CUtensorMapL2promotion l2_promotion() {
-  switch (env_flag("CM_L2PROMO", 256)) {
+CUtensorMapL2promotion promo_of(int v) {
+  switch (v) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   }
 }
+CUtensorMapL2promotion l2_promotion() { return promo_of(env_flag("CM_L2PROMO", 256)); }
+// the diagonal blocks (w = g): a row ends inside the block, so promotion past it only pulls
+// never-read upper-triangle bytes (CM_L2PROMO_DIAG, default none)
+CUtensorMapL2promotion l2_promotion_diag() { return promo_of(env_flag("CM_L2PROMO_DIAG", 0)); }
 
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
@@ -217,8 +221,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   const bool use_tma = a->layout == CM_LAYOUT_DENSE;
-  CUtensorMap tmap;
+  CUtensorMap tmap, tmap_d;
   std::memset(&tmap, 0, sizeof(tmap));
+  std::memset(&tmap_d, 0, sizeof(tmap_d));
   if (use_tma) {
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return fail(CM_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -230,6 +235,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
+    const CUresult r2 = enc(&tmap_d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            l2_promotion_diag(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r2 != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, bulk ? cm2::round_tma_kernel<4, true> : cm2::round_tma_kernel<4, false>,
                                                     256, smem1_for(4));
@@ -346,7 +355,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         std::lock_guard<std::mutex> lock(g->mu);
         e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
         if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
-        void* args[] = {&fp, &tmap};
+        void* args[] = {&fp, &tmap, &tmap_d};
         const bool tr = trace_enabled();
         g_trace.used = 0;
         if (tr) cudaEventRecord(trace_event(0), st);
@@ -401,17 +410,17 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       const size_t sm1 = smem1_for(rp.nt);
       if (bulk) {
         switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 2: cm2::round_tma_kernel<2, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 3: cm2::round_tma_kernel<3, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          default: cm2::round_tma_kernel<4, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 1: cm2::round_tma_kernel<1, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          case 2: cm2::round_tma_kernel<2, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          case 3: cm2::round_tma_kernel<3, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          default: cm2::round_tma_kernel<4, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
         }
       } else {
         switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 2: cm2::round_tma_kernel<2, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          case 3: cm2::round_tma_kernel<3, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
-          default: cm2::round_tma_kernel<4, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap); break;
+          case 1: cm2::round_tma_kernel<1, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          case 2: cm2::round_tma_kernel<2, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          case 3: cm2::round_tma_kernel<3, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
+          default: cm2::round_tma_kernel<4, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
         }
       }
     }

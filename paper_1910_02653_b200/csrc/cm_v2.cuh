@@ -255,7 +255,8 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
 // consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
 // takes queue in `sq` (8 per warp) until the consumer reaches them.
 template <int NT, bool BULK, class Hooks>
-__device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, unsigned char* k1smem,
+__device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const CUtensorMap* tmap_d,
+                                        unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
   constexpr int kSt = k1_stages(NT);
   constexpr uint32_t kStageBytes = (uint32_t)k1_stage_bytes(BULK);
@@ -305,13 +306,15 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     } else if (lane == 0) {
       mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
       void* dst = tiles + (size_t)pstage * kStageBytes;
+      // the diagonal block's rows end inside it: its map has no L2 promotion past the row
+      const CUtensorMap* tm = pw == pg ? tmap_d : tmap;
       if (pol)
-        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
+        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
       else
 #ifdef CM_EXP_L2INPUT
-        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)((p.s_begin + ps) & 63), &bars[pstage]);   // timing experiment
+        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)((p.s_begin + ps) & 63), &bars[pstage]);   // timing experiment
 #else
-        tma_load_3d(dst, tmap, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
+        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
 #endif
     }
     pstage = pstage + 1 == kSt ? 0 : pstage + 1;
@@ -409,7 +412,8 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
 }
 
 template <int NT, bool BULK>
-__global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap,
+                                                                    const __grid_constant__ CUtensorMap tmap_d) {
   extern __shared__ __align__(1024) unsigned char k1raw[];
   unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
   k1_setup<NT, BULK>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
@@ -417,7 +421,7 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
   __shared__ int sq[32][8];
   const K1Plain hk{p.sn, p.n_theta, p.th0, p.cs, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
                    (int)((gridDim.x * blockDim.x) >> 5)};
-  k1_body<NT, BULK>(p, &tmap, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
+  k1_body<NT, BULK>(p, &tmap, &tmap_d, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
 }
 
 
@@ -1047,7 +1051,8 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
 
 template <int NT, bool BULK>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
-                                                                         const __grid_constant__ CUtensorMap tmap) {
+                                                                         const __grid_constant__ CUtensorMap tmap,
+                                                                         const __grid_constant__ CUtensorMap tmap_d) {
   using ET = int32_t;
   constexpr int KF1 = k1_warps(NT);
   extern __shared__ __align__(1024) unsigned char fraw[];
@@ -1072,7 +1077,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   if (warp < KF1) {                                                 // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl};
-    k1_body<NT, BULK>(fp.rp, &tmap, k1smem, warp, sq[warp], hk);
+    k1_body<NT, BULK>(fp.rp, &tmap, &tmap_d, k1smem, warp, sq[warp], hk);
     return;
   }
   // ---- scan (K2) warps
