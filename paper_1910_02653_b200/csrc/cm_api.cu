@@ -91,7 +91,7 @@ EncodeTiledFn encode_tiled() {
 int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
 size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
   const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
-  return (size_t)(s32 ? 4 : 8) * 32 * 32 + (size_t)4 * 32 * spill;
+  return (size_t)(s32 ? 4 : 8) * 32 * 32 + 8192 + (size_t)4 * 32 * spill;   // E, staged masses, spill
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
 // launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).

@@ -625,6 +625,7 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
   // Sn words of the quad holding k and of the quad below (for Sn_{k-1}), loaded a quad ahead
   uint4 quad = lsn ? __ldcg(sn4 + (k0 >> 2)) : make_uint4(0u, 0u, 0u, 0u);
   uint4 nquad = (lsn && (k0 >> 2) > 0) ? __ldcg(sn4 + (k0 >> 2) - 1) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 n2quad = (lsn && (k0 >> 2) > 1) ? __ldcg(sn4 + (k0 >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
   // row 32g's word for k's 32-node block (blocks w < g only; nodes >= 32g are never in S_32g)
   // and, prefetched, for the block below
   uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
@@ -677,8 +678,9 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
     }
     bslot = b1;
     if (u == 0) {                                                   // next node is in the quad below
-      quad = nquad;
-      nquad = (lsn && (k >> 2) >= 2) ? __ldcg(sn4 + (k >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
+      quad = nquad;                                                 // loads run two quads ahead
+      nquad = n2quad;
+      n2quad = (lsn && (k >> 2) >= 3) ? __ldcg(sn4 + (k >> 2) - 3) : make_uint4(0u, 0u, 0u, 0u);
     }
     if ((k & 31) == 0) {                                            // next node is in the block below
       bword = bnext;
@@ -724,6 +726,7 @@ struct ScanCtx {
   const int2* drec;
   const int32_t* qinfo;
   ET* E;                      // [32 stages][32 lanes]
+  int64_t* massbuf;           // [16][32 lanes][2]: the task's checkpoint masses (rows 32g + 2j, +1)
   AView<TM> A;
   bool all_tm;
 };
@@ -741,7 +744,8 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   x.qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
   unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
   x.E = reinterpret_cast<ET*>(wr);
-  x.A.sm = reinterpret_cast<uint32_t*>(x.E + 32 * 32);                 // [slot][lane] (spill part)
+  x.massbuf = reinterpret_cast<int64_t*>(wr + 32 * 32 * sizeof(ET));
+  x.A.sm = reinterpret_cast<uint32_t*>(wr + 32 * 32 * sizeof(ET) + 8192);   // [slot][lane] (spill part)
   x.A.lane = lane;
   x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
   // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
@@ -793,6 +797,15 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   uint32_t* cw = ws + (live ? c : 0) * p.cs;
   const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
   const bool lsn = live && 32 * g + 1 < n;                        // K1 wrote Sn for this group
+  if (live) {  // the group's 32 checkpoint masses (Eq. 6 sums, rows 32g ..) -> shared memory, async
+    const char* msrc = reinterpret_cast<const char*>(cw + block_words(G)) + 256 * (size_t)g;
+    const uint32_t mdst = smem_u32(x.massbuf) + 16u * (uint32_t)lane;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(mdst + 512u * (uint32_t)j), "l"(msrc + 16 * j)
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   if (p.s_mask32) emit_mask<true>(p, ws, n_cand, out_base, p.s_mask32, g, nk, batch0, lane);   // before R overwrites
   // slots: A'_i = Sn_i (Acc_i = 0) for the slotted nodes of the pass.  qinfo[q] = first slot
   // of quad q | (4-bit mask of its slotted nodes) << 16 (slots ascend with the node index).
@@ -855,19 +868,16 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   }
   A.wait_st();                                                    // next task re-fills the slots
   // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
-  const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
+  // the group's checkpoint masses were copied to shared memory at the task start
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
   int64_t pk = INT64_MIN;
-#pragma unroll
-  for (int b0 = 0; b0 < 32; b0 += 8) {                              // 8 loads in flight at a time
-    int64_t mv[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int r = 32 * g + b0 + b;
-      mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
-    }
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (32 * g + b0 + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * (b0 + b) + lane]);
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    const longlong2 mv = reinterpret_cast<const longlong2*>(x.massbuf)[32 * j + lane];
+    const int r = 32 * g + 2 * j;
+    if (r < n) pk = max(pk, (r ? (int64_t)mv.x : 0) + (int64_t)E[32 * (2 * j) + lane]);
+    if (r + 1 < n) pk = max(pk, (int64_t)mv.y + (int64_t)E[32 * (2 * j + 1) + lane]);
   }
   if (live) {
     int64_t* pp = part + 2 * (c * G + g);
