@@ -3,5 +3,7 @@
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
 bench.py's cpu_baseline / --impl reference legs, never by the product package
 (paper_1910_02653_b200).  Shares no code with the CUDA path."""
-from .checkmate_oracle import (Instance, best_per_budget, evaluate, free_matrix,  # noqa: F401
+from .checkmate_oracle import (Instance, best_per_budget, evaluate, evaluate_S, free_matrix,  # noqa: F401
                                masks_u64, memory_U, round_S, two_phase_R)
+from .randomized import (evaluate_randomized, philox4x32_10, round_S_randomized,  # noqa: F401
+                         uniforms)

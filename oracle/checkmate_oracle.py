@@ -148,9 +148,13 @@ def memory_U(inst: Instance, R: np.ndarray, S: np.ndarray, FREE: dict) -> np.nda
 
 def evaluate(inst: Instance, sstar, theta, keep=False) -> dict:
     """One candidate (S*, theta): A1-A6 (+ A8 counters)."""
+    return evaluate_S(inst, round_S(inst, sstar, theta), keep=keep)
+
+
+def evaluate_S(inst: Instance, S: np.ndarray, keep=False) -> dict:
+    """A2-A6 (+ A8 counters) for a rounded S[t][i] (the layout round_S returns)."""
     n = inst.n
     counters = {}
-    S = round_S(inst, sstar, theta)
     R = two_phase_R(inst, S, counters)
     FREE = free_matrix(inst, R, S)
     U = memory_U(inst, R, S, FREE)

@@ -1,0 +1,92 @@
+"""Pins of the oracle's randomized two-phase rounding (R1).
+
+The generator is pinned by the published Philox4x32-10 known-answer vectors; the rounding
+rule by the cases where it must reduce to deterministic rounding, by its mean, and by the
+paper's Appendix D comparison (deterministic rounding is not beaten on average)."""
+import json
+import os
+
+import numpy as np
+
+from oracle import Instance, evaluate, evaluate_randomized, philox4x32_10, round_S, round_S_randomized, uniforms
+from oracle.randomized import philox4x32_10_np, uniform24
+from workloads import graphs as G
+from workloads.sstar import from_binary, gen_sstar
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_philox_known_answers():
+    kat = json.load(open(os.path.join(HERE, "golden", "philox4x32_10_kat.json")))
+    for v in kat["vectors"]:
+        ctr = [int(x, 16) for x in v["ctr"]]
+        key = [int(x, 16) for x in v["key"]]
+        want = [int(x, 16) for x in v["out"]]
+        assert list(philox4x32_10(ctr, key)) == want
+        got = philox4x32_10_np(*[np.array([c], np.uint64) for c in ctr], key[0], key[1])
+        assert [int(g[0]) for g in got] == want
+
+
+def test_uniform_mapping_exact():
+    w = np.array([0, 255, 256, 0xFFFFFFFF, 0x80000000], np.uint32)
+    u = uniform24(w)
+    assert u.dtype == np.float32
+    assert list(u) == [0.0, 0.0, 2.0 ** -24, 1.0 - 2.0 ** -24, 0.5]
+
+
+def test_binary_sstar_equals_deterministic():
+    """S* in {0, 1}: u in [0, 1) gives u < 1 always and u < 0 never, so every sample equals
+    the deterministic rounding at theta = 0.5 (and the whole candidate does)."""
+    g = G.random_training(6, 0.2, 3)
+    inst = Instance.from_graph(g)
+    rng = np.random.default_rng(1)
+    for trial in range(4):
+        S0 = np.tril(rng.random((g.n, g.n)) < 0.4, -1)
+        x = from_binary(S0)
+        det = evaluate(inst, x, 0.5)
+        for j in range(3):
+            assert np.array_equal(round_S_randomized(inst, x, trial, j, 99), round_S(inst, x, 0.5))
+            r = evaluate_randomized(inst, x, trial, j, 99)
+            assert (r["peak"], r["cost"]) == (det["peak"], det["cost"])
+
+
+def test_mean_and_independence():
+    """Pr[S = 1] = S* (PAPER.md:383): constant S* = p gives a fraction p of ones (5 sigma),
+    different samples / S* numbers / seeds give different S, NaN never sets a bit."""
+    n = 96
+    inst = Instance(n, [], np.zeros(n, np.int64), np.zeros(n, np.int64), 0)
+    tri = n * (n - 1) // 2
+    for p in (0.1, 0.5, 0.9):
+        x = np.full((n, n), p, np.float32)
+        S = round_S_randomized(inst, x, 7, 2, 12345)
+        frac = S[1:n + 1, 1:].sum() / tri
+        assert abs(frac - p) < 5 * np.sqrt(p * (1 - p) / tri)
+        assert not np.triu(S[1:n + 1, 1:]).any()          # only i < t
+    x = np.full((n, n), 0.5, np.float32)
+    base = round_S_randomized(inst, x, 7, 0, 1)
+    for s, j, seed in [(7, 1, 1), (8, 0, 1), (7, 0, 2), (7, 4, 1)]:
+        assert not np.array_equal(base, round_S_randomized(inst, x, s, j, seed))
+    x[:] = np.nan
+    assert not round_S_randomized(inst, x, 7, 0, 1).any()
+
+
+def test_uniforms_layout():
+    """u(s, j, t, i) uses counter (i-1, t-1, s, j div 4) and output word j mod 4."""
+    U = uniforms(5, 3, 6, (7 << 32) | 11)
+    for t in range(1, 6):
+        for i in range(1, 6):
+            w = philox4x32_10((i - 1, t - 1, 3, 1), (11, 7))[2]
+            assert U[t - 1, i - 1] == np.float32((w >> 8) * 2.0 ** -24)
+
+
+def test_appendix_d_deterministic_not_worse():
+    """App. D: 'two-phase deterministic rounding produces consistently lower
+    cost schedules' than the mean of randomized ones.  On LP-like S* of the training chain
+    the deterministic cost is at most the mean sampled cost."""
+    g = G.training_chain(8)
+    inst = Instance.from_graph(g)
+    for s in range(3):
+        x = gen_sstar(g, "g1", 5, s, 1)[0]
+        det = evaluate(inst, x, 0.5)["cost"]
+        costs = [evaluate_randomized(inst, x, s, j, 2024)["cost"] for j in range(24)]
+        assert det <= np.mean(costs)
