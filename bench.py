@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
     ap.add_argument("--family", default=None)
+    ap.add_argument("--samples", type=int, default=None,
+                    help="randomized rounding (DESIGN.md R1) with this many samples per S* instead of the thresholds")
     ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
     ap.add_argument("--layout", default="dense", choices=["tri4", "dense"])
     ap.add_argument("--ld", type=int, default=None,
@@ -239,7 +241,7 @@ def main():
     if a.batch:
         batch = a.batch
     seed = 20250101
-    n_theta = len(thetas)
+    n_theta = a.samples if a.samples else len(thetas)
     graph = cm.Graph.from_workload(g)
     ld = a.ld if a.ld else (-(-g.n // 32) * 32 if a.layout == "dense" else None)
     gen = DeviceGenerator(g, fam, seed, layout=a.layout, ld=ld)
@@ -260,9 +262,9 @@ def main():
         key.fill_(cm.CM_KEY_NONE)
         if i is not None:
             k_start[i].record(stream)
-        cm.round_and_evaluate(graph, sstar, th, bu, layout=a.layout, index_base=s_base * n_theta,
-                              total_candidates=total, best_key=key, peak=peak, cost=cost,
-                              stream=stream.cuda_stream)
+        cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
+                              index_base=s_base * n_theta, total_candidates=total, best_key=key, peak=peak,
+                              cost=cost, stream=stream.cuda_stream, samples=a.samples, seed=seed)
         if i is not None:
             k_end[i].record(stream)
         global_best(key)
@@ -299,7 +301,7 @@ def main():
 
     # ---- e2e through the public API with HOST buffers (rank-local, then the same MIN) ----
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and not a.samples:
         # e2e through the public API: pinned HOST buffers in the packed tri4 layout (half the
         # PCIe bytes of dense); H2D copies, kernels and D2H of peak/cost/keys all timed.
         eb = min(a.e2e_batch, batch)
@@ -378,13 +380,15 @@ def main():
             "alg_bytes_per_launch": alg_bytes, "ms_per_launch": path_ms, "kernels": kernels,
             "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
     cpu = None
-    if not a.no_cpu_baseline and world == 1:
+    if not a.no_cpu_baseline and world == 1 and not a.samples:
         cpu = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": elapsed_ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": f"{a.config}: n={g.n}, |E|={len(g.edges)}, {fam} LP-like S* "
-                                   f"({a.layout} fp32), theta={thetas}, {len(budgets)} budgets",
+                                   f"({a.layout} fp32), "
+                                   + (f"randomized rounding, {a.samples} samples per S*" if a.samples
+                                      else f"theta={thetas}") + f", {len(budgets)} budgets",
                        "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
                        "parallelism": f"candidates sharded over {world} GPU(s), NCCL MIN all-reduce of keys",
                        "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush"},

@@ -47,6 +47,8 @@ typedef enum {
 #define CM_LAYOUT_DENSE 0     /* S* row r at sstar + r*ld, ld >= n, ld % 4 == 0 */
 #define CM_LAYOUT_TRI4 1      /* S* row r at sstar + sum_{r'<r} roundup4(r') (packed strict lower triangle) */
 #define CM_KEY_NONE INT64_MAX /* best_key value meaning "no feasible candidate" */
+#define CM_ROUND_THRESHOLD 0  /* cm_eval_args.rounding: deterministic threshold rounding */
+#define CM_ROUND_RANDOMIZED 1 /* cm_eval_args.rounding: randomized rounding (R1) */
 
 /* cudaStream_t without pulling in CUDA headers (same type: struct CUstream_st*). NULL = legacy stream. */
 typedef struct CUstream_st* cm_stream;
@@ -95,6 +97,14 @@ typedef struct {
   void* workspace;          /* device scratch for the stage-sliced S columns, or NULL to use the
                                graph's own (then calls sharing a graph must be stream-ordered) */
   int64_t workspace_bytes;  /* size of `workspace`; >= cm_workspace_bytes(g, 1) */
+  int32_t rounding;         /* a1 rule.  CM_ROUND_THRESHOLD: S = 1[S* > theta_j] (Alg. 2 line 1,
+                               PAPER.md:395), candidate j = threshold j.
+                               CM_ROUND_RANDOMIZED: S = 1[u < S*], Pr[S = 1] = S* (PAPER.md:383, 387),
+                               candidate j = sample j of the S* (n_theta samples, theta unused and
+                               may be NULL); u is the DESIGN.md R1 Philox4x32-10 uniform with
+                               counter (node, row, global S* index, j / 4); index_base must be a
+                               multiple of n_theta (global S* index = index_base / n_theta + s) */
+  uint64_t seed;            /* CM_ROUND_RANDOMIZED: the Philox key (low word, high word) */
 } cm_eval_args;
 
 /*

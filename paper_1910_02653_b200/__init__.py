@@ -12,7 +12,8 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (CM_EMAX, CM_KEY_NONE, CM_LAYOUT_DENSE, CM_LAYOUT_TRI4,  # noqa: F401
+from ._abi import (CM_EMAX, CM_KEY_NONE, CM_LAYOUT_DENSE, CM_LAYOUT_TRI4, CM_ROUND_RANDOMIZED,  # noqa: F401
+                   CM_ROUND_THRESHOLD,
                    CM_NMAX)
 
 _lib = _abi.load()
@@ -115,12 +116,16 @@ def _ptr(t):
 def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str = "dense",
                        n_sstar: int | None = None, ld: int | None = None, stride: int | None = None,
                        index_base: int = 0, total_candidates: int | None = None,
-                       best_key=None, masks: bool = False, peak=None, cost=None, stream=None):
+                       best_key=None, masks: bool = False, peak=None, cost=None, stream=None,
+                       samples: int | None = None, seed: int = 0):
     """cm_round_and_evaluate on device tensors.
 
     sstar : float32 CUDA tensor; dense [N_S, n, ld] or tri4 [N_S, tri4_size(n)] (or any
             buffer with explicit n_sstar / ld / stride).
-    theta : float32 CUDA tensor [N_theta];  budget: int64 CUDA tensor [N_B] or None.
+    theta : float32 CUDA tensor [N_theta] (deterministic rounding, Alg. 2 line 1), or None with
+            ``samples`` = N samples per S* of randomized rounding (R1,
+            Philox key ``seed``).
+    budget: int64 CUDA tensor [N_B] or None.
     Returns dict(peak, cost, best_key, idx_bits, r_mask, s_mask) of CUDA tensors.
     Asynchronous on ``stream`` (default: torch's current stream).
     """
@@ -139,7 +144,10 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
         if stride is None:
             stride = sstar.stride(0) if sstar.dim() == 2 else tri4_size(n)
     dev = sstar.device
-    n_theta = theta.numel()
+    randomized = samples is not None
+    if randomized == (theta is not None):
+        raise ValueError("give exactly one of theta (deterministic) and samples (randomized)")
+    n_theta = int(samples) if randomized else theta.numel()
     n_cand = n_sstar * n_theta
     n_budget = 0 if budget is None else budget.numel()
     if total_candidates is None:
@@ -162,7 +170,9 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     a.ld = int(ld)
     a.sstar_stride = int(stride)
     a.n_theta = n_theta
-    a.theta = theta.data_ptr()
+    a.theta = None if randomized else theta.data_ptr()
+    a.rounding = _abi.CM_ROUND_RANDOMIZED if randomized else _abi.CM_ROUND_THRESHOLD
+    a.seed = int(seed) & ((1 << 64) - 1)
     a.n_budget = n_budget
     a.budget = _ptr(budget)
     a.index_base = int(index_base)

@@ -18,6 +18,8 @@ CM_EMAX = 8192
 CM_LAYOUT_DENSE = 0
 CM_LAYOUT_TRI4 = 1
 CM_KEY_NONE = (1 << 63) - 1
+CM_ROUND_THRESHOLD = 0
+CM_ROUND_RANDOMIZED = 1
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
            "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_key_idx_bits", "cm_decode_key", "cm_status_string",
@@ -44,6 +46,8 @@ class EvalArgs(ctypes.Structure):
         ("s_mask", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_int64),
+        ("rounding", ctypes.c_int32),
+        ("seed", ctypes.c_uint64),
     ]
 
 

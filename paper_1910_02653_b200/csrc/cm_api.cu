@@ -144,6 +144,33 @@ CUtensorMapL2promotion l2_promotion() { return promo_of(env_flag("CM_L2PROMO", 2
 // never-read upper-triangle bytes (CM_L2PROMO_DIAG, default none)
 CUtensorMapL2promotion l2_promotion_diag() { return promo_of(env_flag("CM_L2PROMO_DIAG", 0)); }
 
+const void* round_fn(int nt, bool bulk, bool rnd) {
+#define CM_R(NT) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, true, true>) \
+                              : reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, false, true>)) \
+                      : (bulk ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, true, false>) \
+                              : reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, false, false>)))
+  switch (nt) {
+    case 1: return CM_R(1);
+    case 2: return CM_R(2);
+    case 3: return CM_R(3);
+    default: return CM_R(4);
+  }
+#undef CM_R
+}
+const void* fused_fn(int nt, bool bulk, bool rnd) {
+#define CM_F(NT) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, true>) \
+                              : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, true>)) \
+                      : (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, false>) \
+                              : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, false>)))
+  switch (nt) {
+    case 1: return CM_F(1);
+    case 2: return CM_F(2);
+    case 3: return CM_F(3);
+    default: return CM_F(4);
+  }
+#undef CM_F
+}
+
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
   const int G = (n + 31) / 32;
@@ -195,20 +222,16 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!carve) {
-      for (const void* fn : {reinterpret_cast<const void*>(cm2::round_tma_kernel<1, false>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2, false>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3, false>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4, false>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<1, true>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<2, true>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<3, true>),
-                             reinterpret_cast<const void*>(cm2::round_tma_kernel<4, true>)}) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(cm2::k1_smem_bytes(1, 128 * 32, true), cm2::k1_smem_bytes(4, 128 * 32, true)));
-        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return cuda_fail(e, "carveout(round_tma_kernel)");
-      }
+      for (int nt = 1; nt <= 4; ++nt)
+        for (int bl = 0; bl < 2; ++bl)
+          for (int rd = 0; rd < 2; ++rd) {
+            const void* fn = round_fn(nt, bl != 0, rd != 0);
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max(cm2::k1_smem_bytes(1, 128 * 32, true), cm2::k1_smem_bytes(4, 128 * 32, true)));
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return cuda_fail(e, "carveout(round_tma_kernel)");
+          }
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
@@ -240,8 +263,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                             l2_promotion_diag(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r2 != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, bulk ? cm2::round_tma_kernel<4, true> : cm2::round_tma_kernel<4, false>,
-                                                    256, smem1_for(4));
+  const bool rnd = a->rounding == CM_ROUND_RANDOMIZED;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, round_fn(4, bulk, rnd), 256, smem1_for(4));
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
@@ -262,6 +285,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   rp.nib_entries = g->nib_entries;
   rp.brow = cm2::brow_off(n);
   rp.evict_first = env_flag("CM_EVICT_FIRST", 0);   // measured: -2%
+  rp.key0 = (uint32_t)(a->seed & 0xffffffffu);
+  rp.key1 = (uint32_t)(a->seed >> 32);
+  rp.s0 = (uint32_t)((uint64_t)(a->index_base / a->n_theta) & 0xffffffffu);
 
   cm2::ScanParams sp;
   sp.blob = reinterpret_cast<const uint4*>(g->d_blob2);
@@ -309,17 +335,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
     if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= ws_bytes &&
         total_tasks < (int64_t(1) << 31)) {
-      const void* fn = nullptr;
-      switch (nt * 2 + (bulk ? 1 : 0)) {
-        case 2: fn = reinterpret_cast<const void*>(cm2::fused_kernel<1, false>); break;
-        case 3: fn = reinterpret_cast<const void*>(cm2::fused_kernel<1, true>); break;
-        case 4: fn = reinterpret_cast<const void*>(cm2::fused_kernel<2, false>); break;
-        case 5: fn = reinterpret_cast<const void*>(cm2::fused_kernel<2, true>); break;
-        case 6: fn = reinterpret_cast<const void*>(cm2::fused_kernel<3, false>); break;
-        case 7: fn = reinterpret_cast<const void*>(cm2::fused_kernel<3, true>); break;
-        case 8: fn = reinterpret_cast<const void*>(cm2::fused_kernel<4, false>); break;
-        default: fn = reinterpret_cast<const void*>(cm2::fused_kernel<4, true>); break;
-      }
+      const void* fn = fused_fn(nt, bulk, rnd);
       {
         std::lock_guard<std::mutex> lock(attr_mu);
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);
@@ -408,22 +424,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + wpb - 1) / wpb, (int64_t)g->sm_count));
       const int thr1 = 32 * wpb;
       const size_t sm1 = smem1_for(rp.nt);
-      if (bulk) {
-        switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          case 2: cm2::round_tma_kernel<2, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          case 3: cm2::round_tma_kernel<3, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          default: cm2::round_tma_kernel<4, true><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-        }
-      } else {
-        switch (rp.nt) {
-          case 1: cm2::round_tma_kernel<1, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          case 2: cm2::round_tma_kernel<2, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          case 3: cm2::round_tma_kernel<3, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-          default: cm2::round_tma_kernel<4, false><<<grid1, thr1, sm1, g->st_round>>>(rp, tmap, tmap_d); break;
-        }
-      }
+      void* k1args[] = {&rp, &tmap, &tmap_d};
+      e = cudaLaunchKernel(round_fn(rp.nt, bulk, rnd), dim3((unsigned)grid1), dim3((unsigned)thr1), k1args, sm1, g->st_round);
+      if (e != cudaSuccess) break;
     }
+    if (e != cudaSuccess) break;
     if (tr) cudaEventRecord(trace_event(4 * c + 1), g->st_round);
     e = cudaEventRecord(g->ev_round[b], g->st_round);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, g->ev_round[b], 0);
@@ -768,6 +773,9 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   const int n = g->n;
   if (a->n_sstar < 0 || a->n_theta < 1 || a->n_budget < 0) return fail(CM_EINVAL, "bad counts");
   if (a->layout != CM_LAYOUT_DENSE && a->layout != CM_LAYOUT_TRI4) return fail(CM_EINVAL, "bad layout");
+  if (a->rounding != CM_ROUND_THRESHOLD && a->rounding != CM_ROUND_RANDOMIZED) return fail(CM_EINVAL, "bad rounding");
+  if (a->rounding == CM_ROUND_RANDOMIZED && a->index_base % a->n_theta != 0)
+    return fail(CM_EINVAL, "randomized rounding: index_base must be a multiple of n_theta (samples)");
   int64_t min_stride;
   if (a->layout == CM_LAYOUT_DENSE) {
     if (a->ld < n || (a->ld & 3)) return fail(CM_EINVAL, "ld must be >= n and a multiple of 4");
@@ -783,7 +791,8 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
     if (min_stride > 0 && (!a->sstar || (reinterpret_cast<uintptr_t>(a->sstar) & 15)))
       return fail(CM_EINVAL, "sstar NULL or not 16-byte aligned");
     if (!a->sstar && n > 1) return fail(CM_EINVAL, "sstar NULL");
-    if (!a->theta || !a->peak || !a->cost) return fail(CM_EINVAL, "NULL theta/peak/cost");
+    if ((!a->theta && a->rounding == CM_ROUND_THRESHOLD) || !a->peak || !a->cost)
+      return fail(CM_EINVAL, "NULL theta/peak/cost");
   }
   if (a->n_budget > 0 && (!a->budget || !a->best_key)) return fail(CM_EINVAL, "NULL budget/best_key");
   if (a->n_budget > 4096) return fail(CM_ERANGE, "n_budget > 4096");
@@ -800,6 +809,8 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);
   }
+  if (a->rounding != CM_ROUND_THRESHOLD)
+    return fail(CM_ERANGE, "randomized rounding needs the stage-sliced kernels (graph too large for them)");
 
   const int G = (n + 31) / 32;
   const int tri_words = 16 * G * (G + 1);

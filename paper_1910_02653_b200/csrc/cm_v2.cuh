@@ -120,7 +120,27 @@ struct RoundParams {
   int32_t nib_entries;        // 128 * G
   int32_t brow;               // word offset of brow in a candidate block
   int32_t evict_first;        // S* loads with an L2 evict-first policy
+  // randomized rounding (R1): S = u < S*, u from Philox4x32-10 with counter
+  // (node, row, global S* index, sample / 4) and key (key0, key1); sample j = th0 + j
+  uint32_t key0, key1;
+  uint32_t s0;                // global index of batch S* 0 (mod 2^32)
 };
+
+// Philox4x32-10 (Salmon et al., SC'11); the uniform is (word >> 8) * 2^-24, exact in fp32.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+__device__ __forceinline__ float uniform24(uint32_t w) { return (float)(w >> 8) * 5.9604644775390625e-8f; }
 
 // ---- bulk-async copy + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -238,7 +258,7 @@ struct K1Plain {
 };
 
 // Per-CTA K1 set-up (staged mass table, mbarriers); the caller synchronises the CTA after it.
-template <int NT, bool BULK>
+template <int NT, bool BULK, bool RAND>
 __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1smem, int nwarps1, int tid,
                                          int nthreads) {
   constexpr int kSt = k1_stages(NT);
@@ -254,7 +274,9 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
 // index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
 // consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
 // takes queue in `sq` (8 per warp) until the consumer reaches them.
-template <int NT, bool BULK, class Hooks>
+// RAND: randomized rounding, sample th0 + j instead of threshold th0 + j (one Philox block
+// gives the four samples of a pass).
+template <int NT, bool BULK, bool RAND, class Hooks>
 __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const CUtensorMap* tmap_d,
                                         unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
@@ -274,7 +296,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   }
   float th[NT];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) th[j] = p.theta[p.th0 + j];
+  for (int j = 0; j < NT; ++j) th[j] = RAND ? 0.f : p.theta[p.th0 + j];
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t tiles_u32 = smem_u32(tiles);
@@ -364,12 +386,29 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         const int rem = rq - 32 * w;                                // >= 1: nodes 32w .. rq-1 exist
         const uint32_t rmask = rq >= p.n ? 0u : (rem >= 32 ? FULL : (1u << rem) - 1u);
         uint32_t word[NT];
+        if (RAND) {                                                 // a1 randomized: u < S*
+          uint32_t rw[NT];
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          uint32_t rw = 0u;
+          for (int j = 0; j < NT; ++j) rw[j] = 0u;
+          const uint32_t sg = p.s0 + (uint32_t)(p.s_begin + s);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) rw |= x[q] > th[j] ? (1u << q) : 0u;
-          word[j] = rw & rmask;
+          for (int q = 0; q < 32; ++q) {
+            const uint4 o = philox4x32_10(make_uint4((uint32_t)(32 * w + q), (uint32_t)rq, sg, (uint32_t)(p.th0 >> 2)),
+                                          p.key0, p.key1);
+            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int j = 0; j < NT; ++j) rw[j] |= uniform24(ow[j]) < x[q] ? (1u << q) : 0u;
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) word[j] = rw[j] & rmask;
+        } else {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            uint32_t rw = 0u;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) rw |= x[q] > th[j] ? (1u << q) : 0u;
+            word[j] = rw & rmask;
+          }
         }
         const int node = 32 * w + lane;
         const int brow_at = p.brow + (g + 1) * G + w;               // row 32(g+1) = lane 31's row
@@ -411,17 +450,17 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   }
 }
 
-template <int NT, bool BULK>
+template <int NT, bool BULK, bool RAND>
 __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap,
                                                                     const __grid_constant__ CUtensorMap tmap_d) {
   extern __shared__ __align__(1024) unsigned char k1raw[];
   unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
-  k1_setup<NT, BULK>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
+  k1_setup<NT, BULK, RAND>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
   __syncthreads();
   __shared__ int sq[32][8];
   const K1Plain hk{p.sn, p.n_theta, p.th0, p.cs, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
                    (int)((gridDim.x * blockDim.x) >> 5)};
-  k1_body<NT, BULK>(p, &tmap, &tmap_d, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
+  k1_body<NT, BULK, RAND>(p, &tmap, &tmap_d, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
 }
 
 
@@ -1059,7 +1098,7 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
   return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1023) & ~(size_t)1023;
 }
 
-template <int NT, bool BULK>
+template <int NT, bool BULK, bool RAND>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const __grid_constant__ CUtensorMap tmap_d) {
@@ -1072,7 +1111,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& sp = fp.sp;
-  k1_setup<NT, BULK>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
+  k1_setup<NT, BULK, RAND>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
   for (int i = threadIdx.x; i < sp.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(k2smem)[i] = sp.blob[i];
   if (warp == KF1) {
@@ -1087,7 +1126,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   if (warp < KF1) {                                                 // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl};
-    k1_body<NT, BULK>(fp.rp, &tmap, &tmap_d, k1smem, warp, sq[warp], hk);
+    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &tmap_d, k1smem, warp, sq[warp], hk);
     return;
   }
   // ---- scan (K2) warps

@@ -1,3 +1,3 @@
 // Instances: fused persistent kernels, 4 threshold(s) per pass (see cm_inst.cuh).
 #include "cm_inst.cuh"
-CM_FUSED(4, false) CM_FUSED(4, true)
+CM_FUSED(4, false, false) CM_FUSED(4, true, false)
