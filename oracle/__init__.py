@@ -7,3 +7,4 @@ from .checkmate_oracle import (Instance, best_per_budget, evaluate, evaluate_S, 
                                masks_u64, memory_U, round_S, two_phase_R)
 from .randomized import (evaluate_randomized, philox4x32_10, round_S_randomized,  # noqa: F401
                          uniforms)
+from .max_batch import B_CAP, b_max, max_batch_per_budget  # noqa: F401
