@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
     ap.add_argument("--family", default=None)
+    ap.add_argument("--max-batch", action="store_true",
+                    help="also run the max-batch epilogue (Eq. 13) per budget in the timed step")
     ap.add_argument("--samples", type=int, default=None,
                     help="randomized rounding (DESIGN.md R1) with this many samples per S* instead of the thresholds")
     ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
@@ -251,6 +253,9 @@ def main():
     th = torch.tensor(thetas, dtype=torch.float32, device=dev)
     bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
     key = torch.empty(len(budgets), dtype=torch.int64, device=dev)
+    bkey = torch.empty(len(budgets), dtype=torch.int64, device=dev) if a.max_batch else None
+    from workloads.budgets import eq13_cost_limit
+    limit = eq13_cost_limit(g) if a.max_batch else None
     peak = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
     cost = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
     total = world * batch * n_theta
@@ -260,11 +265,14 @@ def main():
 
     def step(i=None):
         key.fill_(cm.CM_KEY_NONE)
+        if bkey is not None:
+            bkey.fill_(cm.CM_KEY_NONE)
         if i is not None:
             k_start[i].record(stream)
         cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
                               index_base=s_base * n_theta, total_candidates=total, best_key=key, peak=peak,
-                              cost=cost, stream=stream.cuda_stream, samples=a.samples, seed=seed)
+                              cost=cost, stream=stream.cuda_stream, samples=a.samples, seed=seed,
+                              cost_limit=limit, best_batch_key=bkey)
         if i is not None:
             k_end[i].record(stream)
         global_best(key)

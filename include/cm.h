@@ -105,6 +105,14 @@ typedef struct {
                                counter (node, row, global S* index, j / 4); index_base must be a
                                multiple of n_theta (global S* index = index_base / n_theta + s) */
   uint64_t seed;            /* CM_ROUND_RANDOMIZED: the Philox key (low word, high word) */
+  int64_t* best_batch_key;  /* device int64[n_budget] or NULL (off).  Max-batch epilogue (Eq. 13,
+                               PAPER.md:498-511; R2): candidates with cost <= cost_limit
+                               compete per budget b for the largest
+                               B_max = floor((b - ovh) / (peak - ovh)) >= 1, capped at 2^31-1 (peak
+                               is affine in the activation sizes; ovh is held fixed).  In/out:
+                               atomicMin of ((2^31-1 - B_max) << idx_bits) | idx into caller-
+                               initialised CM_KEY_NONE; needs idx_bits <= 32 (else CM_ERANGE) */
+  int64_t cost_limit;       /* Eq. 13's bound 2 sum_fwd C + sum_bwd C, supplied by the caller */
 } cm_eval_args;
 
 /*
@@ -118,6 +126,9 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* args, cm_
 /* Bytes of workspace needed to process `chunk_candidates` candidates per internal chunk
  * (the library splits a batch into chunks that fit the workspace it is given). */
 int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates);
+
+/* max-batch key -> (B_max, idx); CM_KEY_NONE -> (0, -1). */
+void cm_decode_batch_key(int64_t key, int32_t idx_bits, int64_t* b_max, int64_t* idx);
 
 /* idx_bits used by the key packing: number of bits of (total_candidates - 1); 0 when total <= 1. */
 int32_t cm_key_idx_bits(int64_t total_candidates);

@@ -97,6 +97,14 @@ def decode_key(key: int, idx_bits: int):
     return int(c.value), int(i.value)
 
 
+def decode_batch_key(key: int, idx_bits: int):
+    """max-batch key -> (B_max, idx); (0, -1) when nothing fits (cm_decode_batch_key)."""
+    b = ctypes.c_int64()
+    i = ctypes.c_int64()
+    _lib.cm_decode_batch_key(int(key), int(idx_bits), ctypes.byref(b), ctypes.byref(i))
+    return b.value, i.value
+
+
 def debug_trace(max_values: int = 4096):
     """(k1_begin, k1_end, k2_begin, k2_end) per chunk of the last CM_TRACE=1 call, in ms."""
     buf = (ctypes.c_float * max_values)()
@@ -117,7 +125,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
                        n_sstar: int | None = None, ld: int | None = None, stride: int | None = None,
                        index_base: int = 0, total_candidates: int | None = None,
                        best_key=None, masks: bool = False, peak=None, cost=None, stream=None,
-                       samples: int | None = None, seed: int = 0):
+                       samples: int | None = None, seed: int = 0, cost_limit: int | None = None,
+                       best_batch_key=None):
     """cm_round_and_evaluate on device tensors.
 
     sstar : float32 CUDA tensor; dense [N_S, n, ld] or tri4 [N_S, tri4_size(n)] (or any
@@ -126,6 +135,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
             ``samples`` = N samples per S* of randomized rounding (R1,
             Philox key ``seed``).
     budget: int64 CUDA tensor [N_B] or None.
+    cost_limit: with budgets, also run the max-batch epilogue (Eq. 13; the key of the largest
+            B_max per budget among candidates with cost <= cost_limit, in ``best_batch_key``).
     Returns dict(peak, cost, best_key, idx_bits, r_mask, s_mask) of CUDA tensors.
     Asynchronous on ``stream`` (default: torch's current stream).
     """
@@ -158,6 +169,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
         cost = torch.empty(n_cand, dtype=torch.int64, device=dev)
     if best_key is None and n_budget:
         best_key = torch.full((n_budget,), CM_KEY_NONE, dtype=torch.int64, device=dev)
+    if cost_limit is not None and best_batch_key is None and n_budget:
+        best_batch_key = torch.full((n_budget,), CM_KEY_NONE, dtype=torch.int64, device=dev)
     r_mask = s_mask = None
     if masks:
         W = (n + 63) // 64
@@ -173,6 +186,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     a.theta = None if randomized else theta.data_ptr()
     a.rounding = _abi.CM_ROUND_RANDOMIZED if randomized else _abi.CM_ROUND_THRESHOLD
     a.seed = int(seed) & ((1 << 64) - 1)
+    a.best_batch_key = _ptr(best_batch_key)
+    a.cost_limit = int(cost_limit) if cost_limit is not None else 0
     a.n_budget = n_budget
     a.budget = _ptr(budget)
     a.index_base = int(index_base)
@@ -186,7 +201,7 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
         stream = torch.cuda.current_stream(dev).cuda_stream
     _check(_lib.cm_round_and_evaluate(graph.handle, ctypes.byref(a), ctypes.c_void_p(stream)),
            "cm_round_and_evaluate")
-    return {"peak": peak, "cost": cost, "best_key": best_key,
+    return {"peak": peak, "cost": cost, "best_key": best_key, "best_batch_key": best_batch_key,
             "idx_bits": key_idx_bits(total_candidates), "r_mask": r_mask, "s_mask": s_mask}
 
 

@@ -318,6 +318,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   qp.peak = a->peak;
   qp.cost = a->cost;
   qp.best_key = a->best_key;
+  qp.best_batch_key = a->best_batch_key;
+  qp.cost_limit = a->cost_limit;
 
   // ---- fused persistent path (one launch; see cm2::fused_kernel) ----
   if (g->scan32 && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
@@ -490,6 +492,16 @@ const char* cm_status_string(cm_status s) {
 }
 
 const char* cm_last_error(void) { return g_err.c_str(); }
+
+void cm_decode_batch_key(int64_t key, int32_t idx_bits, int64_t* b_max, int64_t* idx) {
+  if (key == CM_KEY_NONE || key < 0) {
+    if (b_max) *b_max = 0;
+    if (idx) *idx = -1;
+    return;
+  }
+  if (b_max) *b_max = ((int64_t(1) << 31) - 1) - (key >> idx_bits);
+  if (idx) *idx = idx_bits ? (key & ((int64_t(1) << idx_bits) - 1)) : 0;
+}
 
 int32_t cm_key_idx_bits(int64_t total_candidates) {
   if (total_candidates <= 1) return 0;
@@ -795,6 +807,8 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
       return fail(CM_EINVAL, "NULL theta/peak/cost");
   }
   if (a->n_budget > 0 && (!a->budget || !a->best_key)) return fail(CM_EINVAL, "NULL budget/best_key");
+  if (a->best_batch_key && cm_key_idx_bits(a->total_candidates) > 32)
+    return fail(CM_ERANGE, "max-batch keys need total_candidates <= 2^32");
   if (a->n_budget > 4096) return fail(CM_ERANGE, "n_budget > 4096");
   const int64_t n_cand = (int64_t)a->n_sstar * a->n_theta;
   if (a->index_base < 0 || a->total_candidates < a->index_base + n_cand)
@@ -809,8 +823,8 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);
   }
-  if (a->rounding != CM_ROUND_THRESHOLD)
-    return fail(CM_ERANGE, "randomized rounding needs the stage-sliced kernels (graph too large for them)");
+  if (a->rounding != CM_ROUND_THRESHOLD || a->best_batch_key)
+    return fail(CM_ERANGE, "randomized rounding / max-batch need the stage-sliced kernels (graph too large for them)");
 
   const int G = (n + 31) / 32;
   const int tri_words = 16 * G * (G + 1);

@@ -985,6 +985,11 @@ struct ReduceParams {
   int64_t* peak;
   int64_t* cost;
   int64_t* best_key;
+  // max-batch epilogue (Eq. 13): candidates with cost <= cost_limit compete
+  // per budget for the largest B_max = floor((b - ovh) / (peak - ovh)) >= 1 (capped at 2^31-1);
+  // key ((2^31-1 - B_max) << idx_bits) | idx, atomicMin into best_batch_key (nullptr: off)
+  int64_t cost_limit;
+  int64_t* best_batch_key;
 };
 
 // peak / cost / a7 keys of candidate c (part rows c, output index out_base + c).
@@ -1004,6 +1009,18 @@ __device__ __forceinline__ void reduce_one(const ReduceParams& p, const int64_t*
     if (pk <= __ldg(p.budget + b)) {
       const int64_t cur = *reinterpret_cast<volatile const int64_t*>(p.best_key + b);
       if (key < cur) atomicMin(reinterpret_cast<long long*>(p.best_key + b), (long long)key);
+    }
+  }
+  if (p.best_batch_key && cs <= p.cost_limit) {
+    constexpr int64_t kCap = (int64_t(1) << 31) - 1;
+    for (int b = 0; b < p.n_budget; ++b) {
+      const int64_t bu = __ldg(p.budget + b);
+      const int64_t bm = bu < p.ovh ? 0 : (pk <= p.ovh ? kCap : min(kCap, (bu - p.ovh) / (pk - p.ovh)));
+      if (bm >= 1) {
+        const int64_t k2 = ((kCap - bm) << p.idx_bits) | (p.index_base + local);
+        const int64_t cur = *reinterpret_cast<volatile const int64_t*>(p.best_batch_key + b);
+        if (k2 < cur) atomicMin(reinterpret_cast<long long*>(p.best_batch_key + b), (long long)k2);
+      }
     }
   }
 }

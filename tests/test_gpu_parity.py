@@ -338,3 +338,36 @@ def test_two_kernel_pipeline(env_var, name, layout):
     x = gen_sstar(g, "mix", 13, 40, 700 if name == "vgg16" else 70)   # vgg16: 2 chunks
     compare(g, x, [0.5, 0.25], B.geometric_grid(g, 8), layout=layout)
     assert cm.debug_last_launches() >= 3
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("name", ["resnet50", "training"])
+def test_max_batch_epilogue(env_var, name, fused):
+    """Max-batch epilogue (Eq. 13, NEXT #4) against the oracle on the oracle's own peaks/costs,
+    on the fused kernel and the two-kernel pipeline."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from oracle import max_batch_per_budget
+    env_var(CM_FUSED=fused)
+    from tests.oracle_helpers import S_all, S_liveness
+    g = G.resnet50() if name == "resnet50" else G.random_training(30, 0.1, 4)
+    # LP-like S* plus two cheap binary schedules (keep-all, liveness: cost sum C <= Eq. 13's
+    # limit) with different peaks, so the epilogue has real choices
+    x = np.concatenate([gen_sstar(g, "g1", 17, 0, 38), from_binary(S_all(g.n))[None],
+                        from_binary(S_liveness(g))[None]])
+    budgets = [int(B.p_live(g) * f) for f in (0.5, 1, 2, 3.5, 8)]   # up to 8x the live peak
+    limit = B.eq13_cost_limit(g)
+    graph = cm.Graph.from_workload(g)
+    thetas = [0.5, 0.3]
+    out = cm.round_and_evaluate(graph, torch.from_numpy(x).cuda(), torch.tensor(thetas, device="cuda"),
+                                torch.tensor(budgets, device="cuda"), cost_limit=limit, index_base=64,
+                                total_candidates=64 + 80)
+    torch.cuda.synchronize()
+    inst, outs = oracle_run(g, x, thetas)
+    peaks = [o["peak"] for o in outs]
+    costs = [o["cost"] for o in outs]
+    assert list(out["peak"].cpu().numpy()) == peaks and list(out["cost"].cpu().numpy()) == costs
+    want = max_batch_per_budget(peaks, costs, budgets, g.ovh, limit, index_base=64)
+    got = [cm.decode_batch_key(int(k), out["idx_bits"]) for k in out["best_batch_key"].cpu().numpy()]
+    assert got == [(b, i) for (b, i) in want]
+    assert any(b > 1 for b, _ in want)                              # a non-trivial instance

@@ -43,3 +43,11 @@ def unet_grid(g_base) -> np.ndarray:
     """Config 4: P_live(base M) x {1, 1.25, 1.5, 2}; candidates run with 5x-scaled M."""
     pl = p_live(g_base)
     return np.array([int(pl * f) for f in (1.0, 1.25, 1.5, 2.0)], np.int64)
+
+
+def eq13_cost_limit(g) -> int:
+    """Eq. 13's right side: 2 sum_{fwd} C_i + sum_{bwd} C_i, with the
+    training graph's forward nodes 0..L-1 and the loss node L counted as forward (R2).
+    Caller-side input of the max-batch epilogue, like the budgets."""
+    c = np.asarray(g.cost, np.int64)
+    return int(2 * c[: g.L + 1].sum() + c[g.L + 1:].sum())
