@@ -8,3 +8,4 @@ from .checkmate_oracle import (Instance, best_per_budget, evaluate, evaluate_S, 
 from .randomized import (evaluate_randomized, philox4x32_10, round_S_randomized,  # noqa: F401
                          uniforms)
 from .max_batch import B_CAP, b_max, max_batch_per_budget  # noqa: F401
+from .plan_sim import generate_plan, hoisted_plan, simulate_plan, spurious_checkpoints  # noqa: F401

@@ -13,6 +13,10 @@ checkmate_oracle.py header for who may import this).
                      start with S_t resident; compute R_t in topological order; after computing
                      v_k, release every value whose last use in the stage is v_k (a computed
                      user, or itself when no user is computed) unless it is kept for stage t+1.
+  hoisted_plan       Alg. 1 plus the code motion of PAPER.md:328: a
+                     checkpoint resident at the start of stage t (S_t) that no computation of
+                     stage t uses and that is not kept for stage t+1 is deallocated at the start
+                     of the stage instead of staying resident until the boundary.
   brute_force_min_R  Enumerate every R (lower triangular, R_{t,t} = 1) satisfying (2) and (3)
                      for a fixed S and return the cheapest (tiny n only).
 """
@@ -30,6 +34,38 @@ def generate_plan(inst, R, FREE):
     r = 0
     P = []
     for t in range(1, n + 1):
+        for k in range(1, n + 1):
+            if R[t, k]:
+                P.append(("compute", t, k, r))
+                REGS[k] = r
+                r += 1
+            for i in inst.DEPS[k] + [k]:
+                if FREE[(i, k)][t - 1]:
+                    P.append(("dealloc", t, REGS[i], i))
+    return P
+
+
+def spurious_checkpoints(inst, R, S, t):
+    """Checkpoints of stage t that are 'unused in a stage' and not kept:
+    i in S_t, no k with R_{t,k} and i in DEPS(k), S_{t+1,i} = 0."""
+    n = inst.n
+    used = set()
+    for k in range(1, n + 1):
+        if R[t, k]:
+            used.update(inst.DEPS[k])
+    return [i for i in range(1, n + 1) if S[t, i] and i not in used and not S[t + 1, i]]
+
+
+def hoisted_plan(inst, R, S, FREE):
+    """Alg. 1 with the spurious checkpoints of every stage deallocated at its start.
+    The register of such a checkpoint is the one of its last computation (REGS[i])."""
+    n = inst.n
+    REGS = [-1] * (n + 1)
+    r = 0
+    P = []
+    for t in range(1, n + 1):
+        for i in spurious_checkpoints(inst, R, S, t):
+            P.append(("dealloc", t, REGS[i], i))
         for k in range(1, n + 1):
             if R[t, k]:
                 P.append(("compute", t, k, r))
