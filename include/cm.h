@@ -145,6 +145,34 @@ int32_t cm_debug_trace(float* out, int32_t max_values);
  * (1 on the fused persistent path; per chunk ceil(n_theta/4) + 2 on the two-kernel pipeline). */
 int32_t cm_debug_last_launches(void);
 
+/*
+ * Execution plans for chosen schedules.  Algorithm 1 "Generate execution
+ * plan" over one candidate's masks: for each stage t, for k = 1..n,
+ * "%r = compute v_k" when R_{t,k}, then "deallocate %REGS[i]" for every i in DEPS(k) u {k} with
+ * FREE_{t,i,k} (Eq. 9).  hoist != 0 adds the code motion of PAPER.md:328: a checkpoint resident
+ * at the start of stage t that no computation of the stage uses and that is not kept for t+1 is
+ * deallocated at the start of the stage.  Host function (no GPU needed).
+ *   n, pred_ptr, pred_idx, mem, mem_overhead   the graph, as in cm_graph_create (host)
+ *   r_mask, s_mask   host [n][W] u64 rows, W = ceil(n/64): the layout cm_round_and_evaluate writes
+ *   out, capacity    statements, stage / node 0-based (stage t <-> row t-1); registers count up
+ *   n_out            receives the number of statements (also when capacity is too small)
+ *   peak_out         receives the plan's peak (stage-boundary semantics: entering stage t exactly
+ *                    the checkpoints S_t are resident; peak after each compute): the Eq. 6-9 peak
+ *                    when hoist = 0, never higher when hoist = 1; may be NULL
+ * CM_EINVAL when the masks violate constraints (2) / (3); CM_ERANGE when capacity < *n_out. */
+typedef struct {
+  int32_t op;     /* CM_OP_COMPUTE or CM_OP_DEALLOC */
+  int32_t stage;  /* 0-based */
+  int32_t node;   /* 0-based v_{node+1}: computed node, or the value deallocated */
+  int32_t reg;    /* virtual register %reg */
+} cm_stmt;
+#define CM_OP_COMPUTE 0
+#define CM_OP_DEALLOC 1
+cm_status cm_emit_plan(int32_t n, const int32_t* pred_ptr, const int32_t* pred_idx, const int64_t* mem,
+                       int64_t mem_overhead, const uint64_t* r_mask, const uint64_t* s_mask, int32_t hoist,
+                       cm_stmt* out, int64_t capacity, int64_t* n_out, int64_t* peak_out);
+const char* cm_plan_last_error(void);
+
 const char* cm_status_string(cm_status s);
 const char* cm_last_error(void);
 

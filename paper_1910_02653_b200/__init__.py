@@ -105,6 +105,33 @@ def decode_batch_key(key: int, idx_bits: int):
     return b.value, i.value
 
 
+CM_OP_COMPUTE, CM_OP_DEALLOC = 0, 1
+
+
+def emit_plan(n, pred_ptr, pred_idx, mem, mem_overhead, r_rows, s_rows, hoist: bool = True):
+    """cm_emit_plan: Alg. 1 execution plan, optionally hoisted,
+    for one candidate's R / S masks (host uint64 [n][W], the layout round_and_evaluate returns).
+    Returns (statements, peak): statements as (op, stage, node, reg) tuples, 0-based."""
+    pred_ptr = np.ascontiguousarray(pred_ptr, np.int32)
+    pred_idx = np.ascontiguousarray(pred_idx, np.int32)
+    mem = np.ascontiguousarray(mem, np.int64)
+    r = np.ascontiguousarray(r_rows).view(np.uint64)
+    s = np.ascontiguousarray(s_rows).view(np.uint64)
+    cap = int(2 * r.size * 64 + 16)
+    while True:
+        out = np.zeros((cap, 4), np.int32)
+        cnt, peak = ctypes.c_int64(), ctypes.c_int64()
+        st = _lib.cm_emit_plan(int(n), pred_ptr.ctypes.data, pred_idx.ctypes.data if pred_idx.size else None,
+                               mem.ctypes.data, int(mem_overhead), r.ctypes.data, s.ctypes.data, int(bool(hoist)),
+                               out.ctypes.data, cap, ctypes.byref(cnt), ctypes.byref(peak))
+        if st == _abi.CM_ERANGE and cnt.value > cap:
+            cap = cnt.value
+            continue
+        if st != _abi.CM_OK:
+            raise CMError(st, "cm_emit_plan: " + _lib.cm_plan_last_error().decode())
+        return [tuple(int(v) for v in row) for row in out[:cnt.value]], int(peak.value)
+
+
 def debug_trace(max_values: int = 4096):
     """(k1_begin, k1_end, k2_begin, k2_end) per chunk of the last CM_TRACE=1 call, in ms."""
     buf = (ctypes.c_float * max_values)()

@@ -22,7 +22,7 @@ CM_ROUND_THRESHOLD = 0
 CM_ROUND_RANDOMIZED = 1
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
-           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string",
+           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
            "cm_last_error")
 
 
@@ -83,6 +83,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_decode_batch_key.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                                         ctypes.POINTER(ctypes.c_int64)]
     lib.cm_decode_batch_key.restype = None
+    lib.cm_emit_plan.argtypes = [ctypes.c_int32, P, P, P, ctypes.c_int64, P, P, ctypes.c_int32, P,
+                                 ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.cm_emit_plan.restype = ctypes.c_int
+    lib.cm_plan_last_error.argtypes = []
+    lib.cm_plan_last_error.restype = ctypes.c_char_p
     lib.cm_status_string.argtypes = [ctypes.c_int]
     lib.cm_status_string.restype = ctypes.c_char_p
     lib.cm_last_error.argtypes = []

@@ -21,7 +21,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-X
 
 LIBS = {
     os.path.join(PKG, "libcheckmate_b200.so"): (
-        sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu"))),
+        sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.cpp"))),
         sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "cm.h")],
         ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc")],
     ),

@@ -371,3 +371,34 @@ def test_max_batch_epilogue(env_var, name, fused):
     got = [cm.decode_batch_key(int(k), out["idx_bits"]) for k in out["best_batch_key"].cpu().numpy()]
     assert got == [(b, i) for (b, i) in want]
     assert any(b > 1 for b, _ in want)                              # a non-trivial instance
+
+
+def test_plan_for_gpu_winners():
+    """NEXT #3 end to end: the GPU picks the per-budget winners and writes their R / S masks;
+    cm_emit_plan turns them into Alg. 1 plans (hoisted), equal to the oracle's."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from oracle import hoisted_plan
+    g = G.vgg16()
+    x = gen_sstar(g, "g1", 23, 0, 24)
+    budgets = B.geometric_grid(g, 4)
+    graph = cm.Graph.from_workload(g)
+    out = cm.round_and_evaluate(graph, torch.from_numpy(x).cuda(), torch.tensor([0.5], device="cuda"),
+                                torch.tensor(budgets, device="cuda"), masks=True)
+    torch.cuda.synchronize()
+    inst = Instance.from_graph(g)
+    ptr, idx = g.pred_csr()
+    checked = 0
+    for key in out["best_key"].cpu().numpy():
+        c, i = cm.decode_key(int(key), out["idx_bits"])
+        if i < 0:
+            continue
+        stmts, peak = cm.emit_plan(g.n, ptr, idx, g.mem, g.ovh, out["r_mask"][i].cpu().numpy(),
+                                   out["s_mask"][i].cpu().numpy(), hoist=True)
+        o = evaluate(inst, x[i], 0.5, keep=True)
+        ref = hoisted_plan(inst, o["R"], o["S"], o["FREE"])
+        assert len(stmts) == len(ref) and peak <= o["peak"] and c == o["cost"]
+        assert [(s[0], s[1], s[2]) for s in stmts] == [
+            ((0, t - 1, a - 1) if op == "compute" else (1, t - 1, b - 1)) for (op, t, a, b) in ref]
+        checked += 1
+    assert checked >= 2
