@@ -9,3 +9,4 @@ from .randomized import (evaluate_randomized, philox4x32_10, round_S_randomized,
                          uniforms)
 from .max_batch import B_CAP, b_max, max_batch_per_budget  # noqa: F401
 from .plan_sim import generate_plan, hoisted_plan, simulate_plan, spurious_checkpoints  # noqa: F401
+from .policies import (S_from_K, articulation_points, evaluate_policy, policy_K)  # noqa: F401
