@@ -173,6 +173,34 @@ cm_status cm_emit_plan(int32_t n, const int32_t* pred_ptr, const int32_t* pred_i
                        cm_stmt* out, int64_t capacity, int64_t* n_out, int64_t* peak_out);
 const char* cm_plan_last_error(void);
 
+/*
+ * Baseline checkpoint policies (Table 1, PAPER.md:103-125, 447-455;
+ * App. B; R3-R5).  For a training graph whose nodes 0..L-1 are the
+ * forward pass (node L the loss, L+1.. the backward pass):
+ *   cm_policy_checkpoints   host: the checkpoint set K (is_checkpoint[L], 0/1) of one policy.
+ *     CM_POLICY_ALL          every forward node (Table 1 "Checkpoint all")
+ *     CM_POLICY_SQRT         Chen et al. sqrt(n) over the forward nodes in topological order
+ *                            (= "Linearized sqrt(n)"; identical on linear graphs): every
+ *                            ceil(sqrt(L))-th node, the last forward node excluded
+ *     CM_POLICY_GREEDY       Chen et al. greedy(b) (= "Linearized greedy"): accumulate M along
+ *                            the forward nodes, checkpoint (and reset) where the sum reaches b
+ *     CM_POLICY_AP_SQRT / _AP_GREEDY  the same over the articulation points of the undirected
+ *                            forward graph plus its first and last node
+ *   cm_policy_sstar         device: the S matrices those sets imply (R3), written as
+ *                            dense 0/1 fp32 S* [n_sets][n][ld] (k_sets: device uint8
+ *                            [n_sets][L]); evaluate them with cm_round_and_evaluate, theta = 0.5.
+ */
+#define CM_POLICY_ALL 0
+#define CM_POLICY_SQRT 1
+#define CM_POLICY_GREEDY 2
+#define CM_POLICY_AP_SQRT 3
+#define CM_POLICY_AP_GREEDY 4
+cm_status cm_policy_checkpoints(int32_t n, int32_t L, const int32_t* pred_ptr, const int32_t* pred_idx,
+                                const int64_t* mem, int32_t policy, int64_t b, uint8_t* is_checkpoint);
+cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const uint8_t* k_sets, float* sstar,
+                          int64_t ld, cm_stream stream);
+const char* cm_policy_last_error(void);
+
 const char* cm_status_string(cm_status s);
 const char* cm_last_error(void);
 

@@ -51,6 +51,7 @@ class Graph:
                                   c.ctypes.data, m.ctypes.data, int(ovh), ctypes.byref(h))
         _check(st, "cm_graph_create")
         self._h = h
+        self.pred_ptr, self.pred_idx, self.cost, self.mem, self.ovh = pp, pi, c, m, int(ovh)
         self.cost_bound = int(_lib.cm_graph_cost_bound(h))
 
     @classmethod
@@ -103,6 +104,42 @@ def decode_batch_key(key: int, idx_bits: int):
     i = ctypes.c_int64()
     _lib.cm_decode_batch_key(int(key), int(idx_bits), ctypes.byref(b), ctypes.byref(i))
     return b.value, i.value
+
+
+POLICIES = {"all": 0, "sqrt": 1, "greedy": 2, "ap_sqrt": 3, "ap_greedy": 4}
+
+
+def policy_checkpoints(graph: Graph, L: int, policy: str, b: int = 0) -> np.ndarray:
+    """cm_policy_checkpoints: the checkpoint set (uint8 [L]) of a baseline policy (Table 1)."""
+    out = np.zeros(int(L), np.uint8)
+    st = _lib.cm_policy_checkpoints(graph.n, int(L), graph.pred_ptr.ctypes.data,
+                                    graph.pred_idx.ctypes.data if graph.pred_idx.size else None,
+                                    graph.mem.ctypes.data, POLICIES[policy], int(b), out.ctypes.data)
+    if st != _abi.CM_OK:
+        raise CMError(st, "cm_policy_checkpoints: " + _lib.cm_policy_last_error().decode())
+    return out
+
+
+def baseline_sweep(graph: Graph, L: int, specs, budget=None, ld: int | None = None, stream=None):
+    """Evaluate baseline policies in one batch: specs = [(policy, b)];
+    the checkpoint sets are built on the host, their S matrices written on the device
+    (cm_policy_sstar) and evaluated like rounded S* (theta = 0.5).  Returns round_and_evaluate's
+    dict plus "k_sets" (uint8 [len(specs)][L])."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ld = int(ld) if ld else -(-graph.n // 32) * 32
+    k = np.stack([policy_checkpoints(graph, L, p, b) for (p, b) in specs])
+    kd = torch.from_numpy(k).to(dev)
+    sstar = torch.empty((len(specs), graph.n, ld), dtype=torch.float32, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(_lib.cm_policy_sstar(graph.handle, int(L), len(specs), kd.data_ptr(), sstar.data_ptr(), ld,
+                                ctypes.c_void_p(stream)), "cm_policy_sstar")
+    out = round_and_evaluate(graph, sstar, torch.tensor([0.5], dtype=torch.float32, device=dev), budget,
+                             stream=stream)
+    out["k_sets"] = k
+    out["sstar"] = sstar
+    return out
 
 
 CM_OP_COMPUTE, CM_OP_DEALLOC = 0, 1

@@ -23,6 +23,7 @@ CM_ROUND_RANDOMIZED = 1
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
            "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
+           "cm_policy_checkpoints", "cm_policy_sstar", "cm_policy_last_error",
            "cm_last_error")
 
 
@@ -88,6 +89,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_emit_plan.restype = ctypes.c_int
     lib.cm_plan_last_error.argtypes = []
     lib.cm_plan_last_error.restype = ctypes.c_char_p
+    lib.cm_policy_checkpoints.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32, ctypes.c_int64, P]
+    lib.cm_policy_checkpoints.restype = ctypes.c_int
+    lib.cm_policy_sstar.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_int64, P]
+    lib.cm_policy_sstar.restype = ctypes.c_int
+    lib.cm_policy_last_error.argtypes = []
+    lib.cm_policy_last_error.restype = ctypes.c_char_p
     lib.cm_status_string.argtypes = [ctypes.c_int]
     lib.cm_status_string.restype = ctypes.c_char_p
     lib.cm_last_error.argtypes = []

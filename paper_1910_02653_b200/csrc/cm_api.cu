@@ -32,6 +32,45 @@ cm_status cuda_fail(cudaError_t e, const char* where) {
 
 }  // namespace
 
+namespace cmp {
+// S of a checkpoint set (R3), one row r of one set per CTA, 0-based: forward nodes
+// 0..L-1, loss L.  i >= L (loss, gradients) or i in K: kept while r <= last(i); other forward
+// nodes: r <= lastF(i), or 2L - tau(i) < r <= last(i) (recomputed at the backward stage of the
+// top tau(i) of i's run of non-checkpoint nodes).  last / lastF from the successor CSR.
+__global__ void policy_sstar_kernel(const int32_t* succ_ptr, const int32_t* succ_idx, int n, int L,
+                                    const uint8_t* k_sets, float* out, int64_t ld) {
+  __shared__ int tau[CM_NMAX];
+  const int r = blockIdx.x, set = blockIdx.y;
+  const uint8_t* K = k_sets + (size_t)set * L;
+  if (threadIdx.x == 0) {
+    int top = -1;
+    for (int v = L - 1; v >= 0; --v) {
+      if (K[v]) top = -1;
+      else if (top < 0) top = v;
+      tau[v] = top;
+    }
+  }
+  __syncthreads();
+  float* row = out + ((size_t)set * n + r) * ld;
+  for (int64_t i = threadIdx.x; i < ld; i += blockDim.x) {
+    float v = 0.f;
+    if (i < r) {
+      int last = (int)i, lastF = (int)i;
+      for (int e = succ_ptr[i]; e < succ_ptr[i + 1]; ++e) {
+        const int j = succ_idx[e];
+        last = max(last, j);
+        if (j <= L) lastF = max(lastF, j);
+      }
+      bool keep;
+      if (i >= L || K[i]) keep = r <= last;
+      else keep = r <= lastF || (2 * L - tau[i] < r && r <= last);
+      v = keep ? 1.f : 0.f;
+    }
+    row[i] = v;
+  }
+}
+}  // namespace cmp
+
 struct cm_graph {
   int32_t n = 0, E = 0;
   int64_t ovh = 0, cost_bound = 0;
@@ -771,6 +810,19 @@ int32_t cm_debug_trace(float* out, int32_t max_values) {
 }
 
 int32_t cm_debug_last_launches(void) { return g_launches; }
+
+cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const uint8_t* k_sets, float* sstar,
+                          int64_t ld, cm_stream stream) {
+  if (!g || L < 1 || L > g->n || n_sets < 0 || n_sets > 65535 || ld < g->n || (n_sets > 0 && (!k_sets || !sstar)))
+    return fail(CM_EINVAL, "cm_policy_sstar: bad arguments");
+  if (n_sets == 0) return CM_OK;
+  const int32_t* gi = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(g->d_blob) + 16 * (size_t)g->n);
+  cmp::policy_sstar_kernel<<<dim3((unsigned)g->n, (unsigned)n_sets), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      gi + g->o_succ_ptr, gi + g->o_succ_idx, g->n, L, k_sets, sstar, ld);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "launch policy_sstar_kernel");
+  return CM_OK;
+}
 
 int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {
   if (!g || chunk_candidates < 1) return -1;

@@ -402,3 +402,35 @@ def test_plan_for_gpu_winners():
             ((0, t - 1, a - 1) if op == "compute" else (1, t - 1, b - 1)) for (op, t, a, b) in ref]
         checked += 1
     assert checked >= 2
+
+
+@pytest.mark.parametrize("name", ["chain", "resnet50", "unet"])
+def test_baseline_policies_on_device(name):
+    """NEXT #2: every policy of Table 1's generalisations with a b-sweep, S written on the
+    device from the checkpoint sets and evaluated in one batch, against the oracle."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from oracle import S_from_K, evaluate_policy
+    g = {"chain": lambda: G.training_chain(20), "resnet50": G.resnet50, "unet": G.unet}[name]()
+    graph = cm.Graph.from_workload(g)
+    fwd = int(g.mem[: g.L].sum())
+    specs = [("all", 0), ("sqrt", 0), ("ap_sqrt", 0)] + \
+            [(p, b) for p in ("greedy", "ap_greedy") for b in (fwd // 40, fwd // 12, fwd // 4)]
+    budgets = B.geometric_grid(g, 6)
+    out = cm.baseline_sweep(graph, g.L, specs, torch.tensor(budgets, device="cuda"))
+    torch.cuda.synchronize()
+    inst = Instance.from_graph(g)
+    names = {"all": "all", "sqrt": "chen_sqrt", "greedy": "chen_greedy", "ap_sqrt": "ap_sqrt",
+             "ap_greedy": "ap_greedy"}
+    sstar = out["sstar"].cpu().numpy()
+    peaks, costs = [], []
+    for c, (p, b) in enumerate(specs):
+        o = evaluate_policy(inst, g.L, names[p], b)
+        S = S_from_K(inst, g.L, o["K"])[1:g.n + 1, 1:]
+        assert np.array_equal(sstar[c][:, :g.n] > 0.5, S), (p, b)
+        assert (int(out["peak"][c]), int(out["cost"][c])) == (o["peak"], o["cost"]), (p, b)
+        peaks.append(o["peak"])
+        costs.append(o["cost"])
+    want = best_per_budget(peaks, costs, budgets)
+    got = [cm.decode_key(int(k), out["idx_bits"]) for k in out["best_key"].cpu().numpy()]
+    assert got == [((w[1], w[0]) if w[0] >= 0 else (-1, -1)) for w in want]
