@@ -220,7 +220,16 @@ __host__ __device__ constexpr int k1_stages(int nt) { return nt == 1 ? CM_K1_STA
 // rows at a 144-byte pitch (one 16-byte chunk of skew per row), so lane l reading 16-byte
 // chunk c of its row hits bank group (l + c) % 8: conflict-free without a swizzle.
 constexpr int kBulkPitch = 144;
-__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 32 * kBulkPitch : 4096; }
+// Dense layout, diagonal blocks (w = g): row 32g+1+l needs only nodes 32g .. 32g+l, so each
+// lane bulk-copies its row's roundup4(l+1) floats into the 144-byte-pitch form instead of the
+// whole 4 KB tile.  The stage then holds either form; 5 KB keeps every stage 1024-byte aligned
+// for the swizzled tensor tiles.  Off by default: measured DRAM reads fell only 292 -> 287 KB
+// per S* (sector / burst granularity of the short rows) while the 32 copy requests per block
+// cost 11 % (16.0 vs 17.9 M cand/s).
+#ifndef CM_DIAG_BULK
+#define CM_DIAG_BULK 0
+#endif
+__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 32 * kBulkPitch : (CM_DIAG_BULK ? 5120 : 4096); }
 __host__ __device__ constexpr size_t k1_bar_off(int nt, bool bulk = false) {
   return ((size_t)k1_warps(nt) * k1_stages(nt) * k1_stage_bytes(bulk) + 1023) & ~(size_t)1023;
 }
@@ -325,6 +334,22 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)lane * kBulkPitch, src, 4u * (uint32_t)len,
                   &bars[pstage]);
       }
+    } else if (CM_DIAG_BULK && pw == pg) {
+      const int l = lane, r = 32 * pg + 1 + l;
+      const int len = r < p.n ? ((l + 4) & ~3) : 0;                 // roundup4(l + 1) floats
+      const uint32_t total = __reduce_add_sync(FULL, (uint32_t)len) * 4u;
+      if (lane == 0) mbar_expect_tx(&bars[pstage], total);
+      __syncwarp();
+      if (len > 0) {
+#ifdef CM_EXP_L2INPUT
+        const int64_t sidx = (p.s_begin + ps) & 63;
+#else
+        const int64_t sidx = p.s_begin + ps;
+#endif
+        const float* src = p.sstar + sidx * p.stride + (int64_t)r * p.ld + 32 * pg;
+        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)l * kBulkPitch, src, 4u * (uint32_t)len,
+                  &bars[pstage]);
+      }
     } else if (lane == 0) {
       mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
       void* dst = tiles + (size_t)pstage * kStageBytes;
@@ -370,13 +395,16 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         issue();
         mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
-        const uint32_t rb = row_base + (uint32_t)cstage * kStageBytes;
+        // diagonal block of the dense layout: per-row bulk copies, 144-byte pitch, no swizzle
+        const bool dbulk = !BULK && CM_DIAG_BULK && w == g;
+        const uint32_t rb = (dbulk ? tiles_u32 + (uint32_t)lane * kBulkPitch : row_base) + (uint32_t)cstage * kStageBytes;
+        const uint32_t sw = dbulk ? 0u : swz;
         float x[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float4 v;
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + (((uint32_t)c << 4) ^ swz)));
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + (((uint32_t)c << 4) ^ sw)));
           x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
         }
         cstage = cstage + 1 == kSt ? 0 : cstage + 1;
