@@ -127,10 +127,10 @@ EncodeTiledFn encode_tiled() {
 }
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
-int64_t cand_bytes(int n) { return 4 * (int64_t)cm2::cand_words(n) + 16 * (int64_t)((n + 31) / 32); }
+int64_t cand_bytes(int n, bool m32) { return 4 * (int64_t)cm2::cand_words(n, m32) + 16 * (int64_t)((n + 31) / 32); }
 size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
   const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
-  return (size_t)(s32 ? 4 : 8) * 32 * 32 + 8192 + (size_t)4 * 32 * spill;   // E, staged masses, spill
+  return (size_t)(s32 ? 4 : 8) * 32 * 32 * 2 + (size_t)4 * 32 * spill;   // E, staged masses, spill
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
 // launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).
@@ -213,12 +213,13 @@ const void* fused_fn(int nt, bool bulk, bool rnd) {
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
   const int n = g->n;
   const int G = (n + 31) / 32;
-  const int cs = cm2::cand_words(n);
+  const bool m32 = g->scan32;                                       // int32 masses in the blocks
+  const int cs = cm2::cand_words(n, m32);
   void* ws = a->workspace ? a->workspace : g->d_ws;
   const int64_t ws_bytes = a->workspace ? a->workspace_bytes : g->ws_bytes;
   if (a->workspace && (reinterpret_cast<uintptr_t>(a->workspace) & 15))
     return fail(CM_EINVAL, "workspace not 16-byte aligned");
-  int64_t cap = ws_bytes / 2 / cand_bytes(n);                       // candidates per chunk buffer
+  int64_t cap = ws_bytes / 2 / cand_bytes(n, m32);                       // candidates per chunk buffer
   cap &= ~int64_t(31);
   if (cap < std::max<int64_t>(32, a->n_theta)) return fail(CM_EINVAL, "workspace too small");
   const int64_t chunk_s = std::min<int64_t>(cap / a->n_theta, 1 << 20);   // S* per chunk
@@ -322,7 +323,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   rp.nib = reinterpret_cast<const int64_t*>(g->d_nib);
   rp.nib32 = reinterpret_cast<const int32_t*>(g->d_nib32);
   rp.nib_entries = g->nib_entries;
-  rp.brow = cm2::brow_off(n);
+  rp.brow = cm2::brow_off(n, m32);
   rp.evict_first = env_flag("CM_EVICT_FIRST", 0);   // measured: -2%
   rp.key0 = (uint32_t)(a->seed & 0xffffffffu);
   rp.key1 = (uint32_t)(a->seed >> 32);
@@ -341,7 +342,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   sp.prefetch = env_flag("CM_PREFETCH", 1);
   sp.cs = cs;
   sp.G = G;
-  sp.brow = cm2::brow_off(n);
+  sp.brow = cm2::brow_off(n, m32);
+  sp.mass_bytes = m32 ? 4 : 8;
   sp.r_mask32 = reinterpret_cast<uint32_t*>(a->r_mask);
   sp.s_mask32 = reinterpret_cast<uint32_t*>(a->s_mask);
   sp.warp_bytes = (int32_t)wb;
@@ -366,7 +368,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
     const size_t wbf = scan_warp_bytes(g->n_slot, true, true, cm2::kFusedTmemCols);
     const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
-    const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n);
+    const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
     const int64_t total_tasks = (units - 1) * (int64_t)G * nt +
                                 (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
@@ -431,7 +433,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   }
 
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
-  const int64_t half = cap * cand_bytes(n);
+  const int64_t half = cap * cand_bytes(n, m32);
   std::lock_guard<std::mutex> lock(g->mu);
   const bool tr = trace_enabled();
   g_trace.used = 0;
@@ -679,7 +681,7 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     g->mscale = gd > 0 ? gd : 1;
     int64_t tot = 0;
     for (int i = 0; i < n; ++i) tot += mem[i] / g->mscale;
-    g->scan32 = tot < (int64_t(1) << 30);
+    g->scan32 = tot < (int64_t(1) << 31);             // E <= sum M (cm_v2.cuh events)
     if (!g->scan32) g->mscale = 1;
   }
   // + node records {(int32) M_k, e0, ndf | adj << 16, slot_k or -1} and far-dependency
@@ -752,7 +754,7 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     }
   }
   if (e == cudaSuccess) {
-    const int64_t per = cand_bytes(n);
+    const int64_t per = cand_bytes(n, g->scan32);
     int64_t want = kDefaultWsBytes;
     if (const char* env = std::getenv("CM_WS_MB")) want = std::max<int64_t>(1, std::atoll(env)) << 20;   // tuning
     g->ws_bytes = std::max<int64_t>(per * 1024, (want / (64 * per)) * 64 * per);
@@ -826,7 +828,7 @@ cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const ui
 
 int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {
   if (!g || chunk_candidates < 1) return -1;
-  return 2 * cand_bytes(g->n) * ((chunk_candidates + 31) & ~int64_t(31));   // two buffers
+  return 2 * cand_bytes(g->n, g->scan32) * ((chunk_candidates + 31) & ~int64_t(31));   // two buffers
 }
 
 int32_t cm_graph_n(const cm_graph* g) { return g ? g->n : -1; }

@@ -45,11 +45,13 @@ __host__ __device__ __forceinline__ int block_words(int G) { return 16 * G * (G 
 // workspace words per candidate: [Sn columns: block_words][mass: n int64][brow: G x G u32]
 // brow row g = the row-form words of S row 32g (bits over nodes), the bit S_t for t = 32g+1
 // that a group-g pass cannot derive from its own Sn columns.
-__host__ __device__ __forceinline__ int cand_words(int n) {
+// m32: the masses are int32 (the int32 scan state: every row mass fits), else int64.
+__host__ __device__ __forceinline__ int mass_words(int n, bool m32) { return m32 ? ((n + 31) & ~31) : 2 * n; }
+__host__ __device__ __forceinline__ int cand_words(int n, bool m32) {
   const int G = (n + 31) / 32;
-  return (block_words(G) + 2 * n + G * G + 3) & ~3;
+  return (block_words(G) + mass_words(n, m32) + G * G + 3) & ~3;
 }
-__host__ __device__ __forceinline__ int brow_off(int n) { return block_words((n + 31) / 32) + 2 * n; }
+__host__ __device__ __forceinline__ int brow_off(int n, bool m32) { return block_words((n + 31) / 32) + mass_words(n, m32); }
 
 __device__ __forceinline__ int64_t row_offset(int layout, int64_t ld, int r) {
   if (layout == 0) return (int64_t)r * ld;
@@ -471,7 +473,10 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
       }
       if (rq < p.n) {
 #pragma unroll
-        for (int j = 0; j < NT; ++j) reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+        for (int j = 0; j < NT; ++j) {
+          if (scaled32) reinterpret_cast<int32_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = (int32_t)mass[j];
+          else reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
+        }
       }
     }
     hk.end(s);
@@ -513,6 +518,7 @@ struct ScanParams {
   int32_t prefetch;           // L2-prefetch the warp's next task
   uint32_t* ws;               // chunk workspace from K1 (cs words per candidate)
   int32_t cs, G, brow;
+  int32_t mass_bytes;         // 4 (int32 state) or 8 per mass entry in a candidate block
   int64_t n_cand;             // candidates in this chunk
   int32_t n_batch;            // ceil(n_cand / 32)
   int64_t* part;              // out: [n_cand][G] x {peak_g - ovh, cost_g}
@@ -571,8 +577,9 @@ struct AView {
 
 // Events of one computing node k: for every stage bit b of x (stage b computes k), in the
 // backward walk, first the frees at k (Eq. 9: the masks f_j with masses m_j, and the i = k
-// self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k, written as
-// max(E_b - frees + M_k, M_k).  NM dependency masks (compile-time).  A round takes up to W
+// self-free sf with M_k), then the compute: E_b = max(E_b - frees, 0) + M_k (E is a memory
+// rise, at most sum M, and every intermediate lies in [-sum M, sum M]: the int32 state needs
+// only sum M / gcd < 2^31).  NM dependency masks (compile-time).  A round takes up to W
 // stage bits of x, highest first (FLO yields the index; stages are independent, so the order
 // is free), and their loads issue together; the width follows the warp's largest per-lane
 // event count (REDUX), so nodes whose lanes compute in one or two stages do not pay for
@@ -600,7 +607,7 @@ __device__ __forceinline__ void event_round(uint32_t& x, uint32_t sf, ET Mk, con
 #pragma unroll
     for (int j = 0; j < NM; ++j)
       if (f[j] & sel[u]) fr += m[j];
-    ev[u] = max(ev[u] - fr + Mk, Mk);
+    ev[u] = max(ev[u] - fr, (ET)0) + Mk;                             // every term within [-sum M, sum M]
   }
 #pragma unroll
   for (int u = 0; u < W; ++u)
@@ -793,7 +800,7 @@ struct ScanCtx {
   const int2* drec;
   const int32_t* qinfo;
   ET* E;                      // [32 stages][32 lanes]
-  int64_t* massbuf;           // [16][32 lanes][2]: the task's checkpoint masses (rows 32g + 2j, +1)
+  ET* massbuf;                // [chunk][32 lanes][16 bytes]: the task's checkpoint masses (rows 32g ..)
   AView<TM> A;
   bool all_tm;
 };
@@ -811,8 +818,8 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   x.qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
   unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
   x.E = reinterpret_cast<ET*>(wr);
-  x.massbuf = reinterpret_cast<int64_t*>(wr + 32 * 32 * sizeof(ET));
-  x.A.sm = reinterpret_cast<uint32_t*>(wr + 32 * 32 * sizeof(ET) + 8192);   // [slot][lane] (spill part)
+  x.massbuf = reinterpret_cast<ET*>(wr + 32 * 32 * sizeof(ET));
+  x.A.sm = reinterpret_cast<uint32_t*>(wr + 2 * 32 * 32 * sizeof(ET));     // [slot][lane] (spill part)
   x.A.lane = lane;
   x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
   // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
@@ -833,10 +840,9 @@ __device__ __forceinline__ void scan_prefetch(const ScanParams& p, const uint32_
     prefetch_l2(col + 128 * (gn + 1) - 4);                          // the block is 16-byte aligned
   }
   prefetch_l2(b + 4 * ((size_t)p.brow + (size_t)gn * G));
-  const unsigned char* ms = b + 4 * (size_t)block_words(G) + 8 * (size_t)(32 * gn);
+  const unsigned char* ms = b + 4 * (size_t)block_words(G) + (size_t)p.mass_bytes * (32 * gn);
   prefetch_l2(ms);
-  prefetch_l2(ms + 128);
-  prefetch_l2(ms + 255);
+  if (p.mass_bytes == 8) prefetch_l2(ms + 128);
 }
 
 // One K2 task: stage group g of the 32 candidates batch0 .. batch0+31 of a buffer `ws` holding
@@ -864,11 +870,14 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   uint32_t* cw = ws + (live ? c : 0) * p.cs;
   const uint4* sn4 = reinterpret_cast<const uint4*>(cw + grp_off(g));
   const bool lsn = live && 32 * g + 1 < n;                        // K1 wrote Sn for this group
-  if (live) {  // the group's 32 checkpoint masses (Eq. 6 sums, rows 32g ..) -> shared memory, async
-    const char* msrc = reinterpret_cast<const char*>(cw + block_words(G)) + 256 * (size_t)g;
+  // the group's 32 checkpoint masses (Eq. 6 sums, rows 32g ..; ET-wide: 128 or 256 bytes)
+  // -> shared memory [chunk j][lane][16 bytes], asynchronously
+  constexpr int kMassChunks = 2 * (int)sizeof(ET);
+  if (live) {
+    const char* msrc = reinterpret_cast<const char*>(cw + block_words(G)) + 32 * sizeof(ET) * (size_t)g;
     const uint32_t mdst = smem_u32(x.massbuf) + 16u * (uint32_t)lane;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < kMassChunks; ++j)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(mdst + 512u * (uint32_t)j), "l"(msrc + 16 * j)
                    : "memory");
   }
@@ -939,12 +948,16 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   int64_t pk = INT64_MIN;
+  constexpr int kPer = 16 / (int)sizeof(ET);                        // masses per 16-byte chunk
 #pragma unroll 4
-  for (int j = 0; j < 16; ++j) {
-    const longlong2 mv = reinterpret_cast<const longlong2*>(x.massbuf)[32 * j + lane];
-    const int r = 32 * g + 2 * j;
-    if (r < n) pk = max(pk, (r ? (int64_t)mv.x : 0) + (int64_t)E[32 * (2 * j) + lane]);
-    if (r + 1 < n) pk = max(pk, (int64_t)mv.y + (int64_t)E[32 * (2 * j + 1) + lane]);
+  for (int j = 0; j < kMassChunks; ++j) {
+    ET mv[kPer];
+    *reinterpret_cast<uint4*>(mv) = reinterpret_cast<const uint4*>(x.massbuf)[32 * j + lane];
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int b = kPer * j + e, r = 32 * g + b;
+      if (r < n) pk = max(pk, (r ? (int64_t)mv[e] : 0) + (int64_t)E[32 * b + lane]);
+    }
   }
   if (live) {
     int64_t* pp = part + 2 * (c * G + g);
@@ -1215,7 +1228,11 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
     warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
     scan_prefetch(sp, ws, ncand, g, (int64_t)batch * 32 + lane);
+#ifndef CM_NO_NEXT_PREFETCH
     if ((int64_t)t_next < fp.total_tasks) {
+#else
+    if (false) {
+#endif
       const Task e = decode(t_next);
       bool ready = false;
       if (lane == 0) ready = ld_acquire(fp.ctl + 1 + e.slot) >= (uint32_t)(32 * e.k + e.ns);

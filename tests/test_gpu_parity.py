@@ -434,3 +434,16 @@ def test_baseline_policies_on_device(name):
     want = best_per_budget(peaks, costs, budgets)
     got = [cm.decode_key(int(k), out["idx_bits"]) for k in out["best_key"].cpu().numpy()]
     assert got == [((w[1], w[0]) if w[0] >= 0 else (-1, -1)) for w in want]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_int32_state_near_limit(layout):
+    """sum M / gcd(M) just below 2^31: still the int32 scan state (E <= sum M, every
+    intermediate within [-sum M, sum M]); exact against the oracle."""
+    g = G.random_training(24, 0.15, 8)
+    rng = np.random.default_rng(8)
+    w = rng.integers(1, 1000, g.n).astype(np.int64)
+    g.mem = (w * ((2 ** 31 - 1) // int(w.sum()))) * 3           # gcd 3 (or a multiple), sum/gcd < 2^31
+    assert int(g.mem.sum()) // 3 < 2 ** 31
+    x = gen_sstar(g, "mix", 19, 0, 8)
+    compare(g, x, [0.5, 0.2], [B.p_floor(g), B.p_live(g)], masks=True, layout=layout)
