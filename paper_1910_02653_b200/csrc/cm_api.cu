@@ -303,6 +303,24 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                             l2_promotion_diag(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r2 != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
+  // tri4: a 2-D map whose rows are the batch's 16-byte units (stride 16 B: overlapping 128-byte
+  // rows), read by tile::gather4; every row it can address lies inside the batch buffer.
+  int32_t g4 = 0;
+  if (bulk && env_flag("CM_GATHER4", 1)) {
+    const int64_t floats = (int64_t)a->n_sstar * a->sstar_stride;
+    const int64_t rows = floats >= 32 ? (floats - 32) / 4 + 1 : 0;
+    EncodeTiledFn enc = encode_tiled();
+    if (enc && rows >= 1 && rows < (int64_t(1) << 31) - 64) {
+      const cuuint64_t dims[2] = {32, (cuuint64_t)rows};
+      const cuuint64_t strides[1] = {16};
+      const cuuint32_t box[2] = {32, 1};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a->sstar), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      g4 = r == CUDA_SUCCESS ? 1 : 0;
+    }
+  }
   const bool rnd = a->rounding == CM_ROUND_RANDOMIZED;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, round_fn(4, bulk, rnd), 256, smem1_for(4));
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
@@ -325,6 +343,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   rp.nib_entries = g->nib_entries;
   rp.brow = cm2::brow_off(n, m32);
   rp.evict_first = env_flag("CM_EVICT_FIRST", 0);   // measured: -2%
+  rp.g4 = g4;
+  // an S* whose rows' 128-byte windows stay inside the buffer: (s + 1) stride + 32 <= N stride
+  rp.g4_end = a->sstar_stride > 0 ? std::max<int64_t>(0, (int64_t)a->n_sstar - (32 + a->sstar_stride - 1) / a->sstar_stride)
+                                  : 0;
   rp.key0 = (uint32_t)(a->seed & 0xffffffffu);
   rp.key1 = (uint32_t)(a->seed >> 32);
   rp.s0 = (uint32_t)((uint64_t)(a->index_base / a->n_theta) & 0xffffffffu);

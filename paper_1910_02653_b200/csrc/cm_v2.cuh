@@ -126,6 +126,8 @@ struct RoundParams {
   // (node, row, global S* index, sample / 4) and key (key0, key1); sample j = th0 + j
   uint32_t key0, key1;
   uint32_t s0;                // global index of batch S* 0 (mod 2^32)
+  int32_t g4;                 // tri4: tile::gather4 through the 16-byte-unit tensor map (else per-row copies)
+  int64_t g4_end;             // batch-relative: S* from here on take per-row copies (window past the end)
 };
 
 // Philox4x32-10 (Salmon et al., SC'11); the uniform is (word >> 8) * 2^-24, exact in fp32.
@@ -187,6 +189,13 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       :: "r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// tile::gather4 (sm_100a): four rows y0..y3 of a 2-D tensor map, box {32, 1}, into dst.
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, int y0, int y1, int y2, int y3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(dst), "l"(tmap), "r"(0), "r"(y0), "r"(y1), "r"(y2), "r"(y3), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(ptr));
 }
@@ -231,7 +240,9 @@ constexpr int kBulkPitch = 144;
 #ifndef CM_DIAG_BULK
 #define CM_DIAG_BULK 0
 #endif
-__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 32 * kBulkPitch : (CM_DIAG_BULK ? 5120 : 4096); }
+// tri4 (bulk): 5 KB so a stage holds either the swizzled 4 KB gather4 tile (1024-aligned) or
+// the 144-byte-pitch per-row form of the fallback.
+__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 5120 : (CM_DIAG_BULK ? 5120 : 4096); }
 __host__ __device__ constexpr size_t k1_bar_off(int nt, bool bulk = false) {
   return ((size_t)k1_warps(nt) * k1_stages(nt) * k1_stage_bytes(bulk) + 1023) & ~(size_t)1023;
 }
@@ -311,9 +322,12 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t tiles_u32 = smem_u32(tiles);
-  const uint32_t row_base = tiles_u32 + (uint32_t)lane * (BULK ? (uint32_t)kBulkPitch : 128u);   // stage 0, this lane's row
+  // tri4 read by gather4 lands in the same 128-byte-swizzled form as the dense tensor tiles.
+  // The batch's last S* (the last ceil(32 / stride) for tiny graphs) cannot use it -- a row's
+  // 128-byte window may run past the buffer -- so those take per-row bulk copies of exactly the
+  // stored floats into the 144-byte-pitch form.
+  auto pitched_of = [&](int s_rel) { return BULK && (!p.g4 || p.s_begin + s_rel >= p.g4_end); };
   const uint64_t pol = (!BULK && p.evict_first) ? l2_evict_first_policy() : 0ull;
-  const uint32_t swz = BULK ? 0u : (uint32_t)(lane & 7) << 4;
 
   // Producer cursor (ps, pg, pw) runs kSt-1 blocks ahead of the consumer.  No proxy
   // fence before re-filling a stage: its previous contents were consumed (ballots issued on
@@ -324,7 +338,21 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   ++qhead;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
-    if (BULK) {
+    if (BULK && !pitched_of(ps)) {
+      // tri4 through a 2-D tensor map whose "rows" are the batch's 16-byte units (an
+      // overlapping stride): block row r = 32 pg + 1 + lane starts at unit (offset of S* ps +
+      // offset of row r + 32 pw) / 4.  Eight tile::gather4 loads (lanes 0, 4, .., 28) each
+      // place four rows, so the stage holds the swizzled 32 x 32 tile of the dense path, and
+      // the bytes fetched are the stored triangle itself (plus the next rows' heads where a
+      // row ends inside the block, which other blocks read anyway).
+      const int r = 32 * pg + 1 + lane;
+      const int y = (int)((((p.s_begin + ps) * p.stride) + row_offset(1, 0, r) + 32 * pw) >> 2);
+      const int y1 = __shfl_down_sync(FULL, y, 1), y2 = __shfl_down_sync(FULL, y, 2), y3 = __shfl_down_sync(FULL, y, 3);
+      if (lane == 0) mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
+      __syncwarp();
+      if ((lane & 3) == 0)
+        tma_gather4(tiles_u32 + (uint32_t)pstage * kStageBytes + 128u * (uint32_t)lane, tmap, y, y1, y2, y3, &bars[pstage]);
+    } else if (BULK) {
       // this lane's row r = 32 pg + 1 + lane, nodes 32 pw .. : the stored part of the block
       const int r = 32 * pg + 1 + lane;
       const int len = r < p.n ? min(32, ((r + 3) & ~3) - 32 * pw) : 0;   // floats, % 4 == 0, > 0 if r < n
@@ -399,8 +427,9 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         phase_bits ^= 1u << cstage;
         // diagonal block of the dense layout: per-row bulk copies, 144-byte pitch, no swizzle
         const bool dbulk = !BULK && CM_DIAG_BULK && w == g;
-        const uint32_t rb = (dbulk ? tiles_u32 + (uint32_t)lane * kBulkPitch : row_base) + (uint32_t)cstage * kStageBytes;
-        const uint32_t sw = dbulk ? 0u : swz;
+        const bool pitched = dbulk || pitched_of(s);
+        const uint32_t rb = tiles_u32 + (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : 128u) + (uint32_t)cstage * kStageBytes;
+        const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
         float x[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
