@@ -130,6 +130,21 @@ struct RoundParams {
   int64_t g4_end;             // batch-relative: S* from here on take per-row copies (window past the end)
 };
 
+// w |= (x[q] > th) << q for q = Q0 .. Q0+15 (strict fp32 compare, NaN -> 0): a setp and a
+// predicated or per element, which ptxas emits as FSETP + @P VIADD (the bits are disjoint).
+template <int Q>
+__device__ __forceinline__ void pack_gt1(uint32_t& w, float v, float th) {
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+      : "+r"(w) : "f"(v), "f"(th), "n"(1u << Q));
+}
+template <int Q0, int K = 0>
+__device__ __forceinline__ void pack_gt(uint32_t& w, const float* x, float th) {
+  if constexpr (K < 16) {
+    pack_gt1<Q0 + K>(w, x[Q0 + K], th);
+    pack_gt<Q0, K + 1>(w, x, th);
+  }
+}
+
 // Philox4x32-10 (Salmon et al., SC'11); the uniform is (word >> 8) * 2^-24, exact in fp32.
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -463,10 +478,11 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         } else {
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
-            uint32_t rw = 0u;
-#pragma unroll
-            for (int q = 0; q < 32; ++q) rw |= x[q] > th[j] ? (1u << q) : 0u;
-            word[j] = rw & rmask;
+            // two independent chains of (FSETP, predicated add): 2 instructions per element
+            uint32_t lo = 0u, hi = 0u;
+            pack_gt<0>(lo, x, th[j]);
+            pack_gt<16>(hi, x, th[j]);
+            word[j] = (lo | hi) & rmask;
           }
         }
         const int node = 32 * w + lane;
