@@ -130,7 +130,7 @@ EncodeTiledFn encode_tiled() {
 int64_t cand_bytes(int n, bool m32) { return 4 * (int64_t)cm2::cand_words(n, m32) + 16 * (int64_t)((n + 31) / 32); }
 size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
   const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
-  return (size_t)(s32 ? 4 : 8) * 32 * 32 * 2 + (size_t)4 * 32 * spill;   // E, staged masses, spill
+  return (size_t)(s32 ? 4 * 32 * 32 * 2 : 8 * 32 * 32) + (size_t)4 * 32 * spill;   // E (+ staged int32 masses), spill
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
 // launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).
@@ -196,16 +196,24 @@ const void* round_fn(int nt, bool bulk, bool rnd) {
   }
 #undef CM_R
 }
-const void* fused_fn(int nt, bool bulk, bool rnd) {
-#define CM_F(NT) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, true>) \
-                              : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, true>)) \
-                      : (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, false>) \
-                              : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, false>)))
+const void* fused_fn(int nt, bool bulk, bool rnd, bool s32) {
+#define CM_F(NT, ET) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, true, int32_t>) \
+                                  : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, true, int32_t>)) \
+                          : (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, false, ET>) \
+                                  : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, false, ET>)))
+  if (s32) {
+    switch (nt) {
+      case 1: return CM_F(1, int32_t);
+      case 2: return CM_F(2, int32_t);
+      case 3: return CM_F(3, int32_t);
+      default: return CM_F(4, int32_t);
+    }
+  }
   switch (nt) {
-    case 1: return CM_F(1);
-    case 2: return CM_F(2);
-    case 3: return CM_F(3);
-    default: return CM_F(4);
+    case 1: return CM_F(1, int64_t);
+    case 2: return CM_F(2, int64_t);
+    case 3: return CM_F(3, int64_t);
+    default: return CM_F(4, int64_t);
   }
 #undef CM_F
 }
@@ -385,10 +393,10 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   qp.cost_limit = a->cost_limit;
 
   // ---- fused persistent path (one launch; see cm2::fused_kernel) ----
-  if (g->scan32 && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
+  if ((g->scan32 || !rnd) && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
     const int nt = a->n_theta;
     const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
-    const size_t wbf = scan_warp_bytes(g->n_slot, true, true, cm2::kFusedTmemCols);
+    const size_t wbf = scan_warp_bytes(g->n_slot, g->scan32, true, cm2::kFusedTmemCols);
     const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
@@ -400,7 +408,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
     if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= ws_bytes &&
         total_tasks < (int64_t(1) << 31)) {
-      const void* fn = fused_fn(nt, bulk, rnd);
+      const void* fn = fused_fn(nt, bulk, rnd, g->scan32);
       {
         std::lock_guard<std::mutex> lock(attr_mu);
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);

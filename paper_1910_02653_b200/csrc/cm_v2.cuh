@@ -863,8 +863,8 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   x.qinfo = reinterpret_cast<const int32_t*>(smem + p.o_qinfo);
   unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
   x.E = reinterpret_cast<ET*>(wr);
-  x.massbuf = reinterpret_cast<ET*>(wr + 32 * 32 * sizeof(ET));
-  x.A.sm = reinterpret_cast<uint32_t*>(wr + 2 * 32 * 32 * sizeof(ET));     // [slot][lane] (spill part)
+  x.massbuf = reinterpret_cast<ET*>(wr + 32 * 32 * sizeof(ET));           // int32 state only
+  x.A.sm = reinterpret_cast<uint32_t*>(wr + (sizeof(ET) == 4 ? 2 : 1) * 32 * 32 * sizeof(ET));   // [slot][lane] (spill part)
   x.A.lane = lane;
   x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
   // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
@@ -918,7 +918,8 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   // the group's 32 checkpoint masses (Eq. 6 sums, rows 32g ..; ET-wide: 128 or 256 bytes)
   // -> shared memory [chunk j][lane][16 bytes], asynchronously
   constexpr int kMassChunks = 2 * (int)sizeof(ET);
-  if (live) {
+  constexpr bool kStageMass = sizeof(ET) == 4;                      // int64: read at the end (smem)
+  if (kStageMass && live) {
     const char* msrc = reinterpret_cast<const char*>(cw + block_words(G)) + 32 * sizeof(ET) * (size_t)g;
     const uint32_t mdst = smem_u32(x.massbuf) + 16u * (uint32_t)lane;
 #pragma unroll
@@ -990,18 +991,34 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   A.wait_st();                                                    // next task re-fills the slots
   // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
   // the group's checkpoint masses were copied to shared memory at the task start
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
   int64_t pk = INT64_MIN;
-  constexpr int kPer = 16 / (int)sizeof(ET);                        // masses per 16-byte chunk
+  if (kStageMass) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    constexpr int kPer = 16 / (int)sizeof(ET);                      // masses per 16-byte chunk
 #pragma unroll 4
-  for (int j = 0; j < kMassChunks; ++j) {
-    ET mv[kPer];
-    *reinterpret_cast<uint4*>(mv) = reinterpret_cast<const uint4*>(x.massbuf)[32 * j + lane];
+    for (int j = 0; j < kMassChunks; ++j) {
+      ET mv[kPer];
+      *reinterpret_cast<uint4*>(mv) = reinterpret_cast<const uint4*>(x.massbuf)[32 * j + lane];
 #pragma unroll
-    for (int e = 0; e < kPer; ++e) {
-      const int b = kPer * j + e, r = 32 * g + b;
-      if (r < n) pk = max(pk, (r ? (int64_t)mv[e] : 0) + (int64_t)E[32 * b + lane]);
+      for (int e = 0; e < kPer; ++e) {
+        const int b = kPer * j + e, r = 32 * g + b;
+        if (r < n) pk = max(pk, (r ? (int64_t)mv[e] : 0) + (int64_t)E[32 * b + lane]);
+      }
+    }
+  } else {
+    const int64_t* mass = reinterpret_cast<const int64_t*>(cw + block_words(G));
+#pragma unroll
+    for (int b0 = 0; b0 < 32; b0 += 8) {                            // 8 loads in flight at a time
+      int64_t mv[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int r = 32 * g + b0 + b;
+        mv[b] = (r && r < n && live) ? __ldcg(mass + r) : 0;
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (32 * g + b0 + b < n) pk = max(pk, mv[b] + (int64_t)E[32 * (b0 + b) + lane]);
     }
   }
   if (live) {
@@ -1201,11 +1218,11 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
   return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1023) & ~(size_t)1023;
 }
 
-template <int NT, bool BULK, bool RAND>
+// ET: the scan state (int32 when sum M / gcd < 2^31, else int64).
+template <int NT, bool BULK, bool RAND, typename ET>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const __grid_constant__ CUtensorMap tmap_d) {
-  using ET = int32_t;
   constexpr int KF1 = k1_warps(NT);
   extern __shared__ __align__(1024) unsigned char fraw[];
   unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
