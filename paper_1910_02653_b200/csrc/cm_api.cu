@@ -292,24 +292,26 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   const bool use_tma = a->layout == CM_LAYOUT_DENSE;
-  CUtensorMap tmap, tmap_d;
+  CUtensorMap tmap;
+  cm2::DiagMaps dmaps;
   std::memset(&tmap, 0, sizeof(tmap));
-  std::memset(&tmap_d, 0, sizeof(tmap_d));
+  std::memset(&dmaps, 0, sizeof(dmaps));
   if (use_tma) {
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return fail(CM_ECUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[3] = {(cuuint64_t)a->ld, (cuuint64_t)n, (cuuint64_t)a->n_sstar};
     const cuuint64_t strides[2] = {(cuuint64_t)a->ld * 4, (cuuint64_t)a->sstar_stride * 4};
     const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t box_up[3] = {16, 16, 1};
+    const cuuint32_t box_lo[3] = {32, 16, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
-    const CUresult r2 = enc(&tmap_d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides,
-                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            l2_promotion_diag(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r2 != CUDA_SUCCESS) return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
+    auto mk = [&](CUtensorMap* m, const cuuint32_t* bx, CUtensorMapL2promotion pr) {
+      return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides, bx, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    if (mk(&tmap, box, l2_promotion()) != CUDA_SUCCESS || mk(&dmaps.upper, box_up, l2_promotion_diag()) != CUDA_SUCCESS ||
+        mk(&dmaps.lower, CM_DIAG_SPLIT ? box_lo : box, l2_promotion_diag()) != CUDA_SUCCESS)
+      return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
   // tri4: a 2-D map whose rows are the batch's 16-byte units (stride 16 B: overlapping 128-byte
   // rows), read by tile::gather4; every row it can address lies inside the batch buffer.
@@ -444,7 +446,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         std::lock_guard<std::mutex> lock(g->mu);
         e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
         if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
-        void* args[] = {&fp, &tmap, &tmap_d};
+        void* args[] = {&fp, &tmap, &dmaps};
         const bool tr = trace_enabled();
         g_trace.used = 0;
         if (tr) cudaEventRecord(trace_event(0), st);
@@ -497,7 +499,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((warps1 + wpb - 1) / wpb, (int64_t)g->sm_count));
       const int thr1 = 32 * wpb;
       const size_t sm1 = smem1_for(rp.nt);
-      void* k1args[] = {&rp, &tmap, &tmap_d};
+      void* k1args[] = {&rp, &tmap, &dmaps};
       e = cudaLaunchKernel(round_fn(rp.nt, bulk, rnd), dim3((unsigned)grid1), dim3((unsigned)thr1), k1args, sm1, g->st_round);
       if (e != cudaSuccess) break;
     }

@@ -3,9 +3,9 @@
 #pragma once
 #include "cm_v2.cuh"
 
-#define CM_ROUND(NT, BULK, RAND) template __global__ void cm2::round_tma_kernel<NT, BULK, RAND>(const cm2::RoundParams, const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+#define CM_ROUND(NT, BULK, RAND) template __global__ void cm2::round_tma_kernel<NT, BULK, RAND>(const cm2::RoundParams, const __grid_constant__ CUtensorMap, const __grid_constant__ cm2::DiagMaps);
 #define CM_SCAN(ET, TM) template __global__ void cm2::scan_kernel<ET, TM>(const cm2::ScanParams);
-#define CM_FUSED(NT, BULK, RAND, ET) template __global__ void cm2::fused_kernel<NT, BULK, RAND, ET>(const cm2::FusedParams, const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+#define CM_FUSED(NT, BULK, RAND, ET) template __global__ void cm2::fused_kernel<NT, BULK, RAND, ET>(const cm2::FusedParams, const __grid_constant__ CUtensorMap, const __grid_constant__ cm2::DiagMaps);
 #define CM_REDUCE template __global__ void cm2::reduce_kernel<0>(const cm2::ReduceParams);
 
 #ifdef CM_API_TU

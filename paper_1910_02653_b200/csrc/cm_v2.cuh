@@ -307,6 +307,21 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Dense diagonal blocks (w = g) in two loads: rows 32g+1..32g+16 need nodes < 32g+16 only
+// (box {16, 16}; with the 128-byte swizzle it fills logical chunks 0-3 of rows 0-15 of the
+// tile, exactly as a full box would), rows 32g+17..32g+32 the whole width (box {32, 16} at
+// row 16).  3 KB instead of 4 KB; neither map promotes past the block (the rows end there).
+// Off by default (CM_DIAG_SPLIT): measured DRAM reads fell only 1.4 KB per S* -- the 256-byte
+// L2 promotion of block w = g-1 has already fetched the diagonal rows' 128 bytes -- and the
+// second request cost ~0.7 %.  With it off, `lower` is the full {32, 32} box without promotion.
+#ifndef CM_DIAG_SPLIT
+#define CM_DIAG_SPLIT 0
+#endif
+struct DiagMaps {
+  CUtensorMap upper;   // box {16 nodes, 16 rows}
+  CUtensorMap lower;   // box {32 nodes, 16 rows}
+};
+
 // K1 body of one warp: S* s = hk.first(), hk.next(s), ... while < s_count; wl = the warp's
 // index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
 // consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
@@ -314,7 +329,7 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
 // RAND: randomized rounding, sample th0 + j instead of threshold th0 + j (one Philox block
 // gives the four samples of a pass).
 template <int NT, bool BULK, bool RAND, class Hooks>
-__device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const CUtensorMap* tmap_d,
+__device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const DiagMaps* dmaps,
                                         unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
   constexpr int kSt = k1_stages(NT);
@@ -395,11 +410,20 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)l * kBulkPitch, src, 4u * (uint32_t)len,
                   &bars[pstage]);
       }
+    } else if (CM_DIAG_SPLIT && lane == 0 && pw == pg) {
+#ifdef CM_EXP_L2INPUT
+      const int z = (int)((p.s_begin + ps) & 63);
+#else
+      const int z = (int)(p.s_begin + ps);
+#endif
+      mbar_expect_tx(&bars[pstage], 3u * 1024u);
+      unsigned char* dst = tiles + (size_t)pstage * kStageBytes;
+      tma_load_3d(dst, &dmaps->upper, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
+      tma_load_3d(dst + 2048, &dmaps->lower, 32 * pw, 32 * pg + 17, z, &bars[pstage]);
     } else if (lane == 0) {
       mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
       void* dst = tiles + (size_t)pstage * kStageBytes;
-      // the diagonal block's rows end inside it: its map has no L2 promotion past the row
-      const CUtensorMap* tm = pw == pg ? tmap_d : tmap;
+      const CUtensorMap* tm = pw == pg ? &dmaps->lower : tmap;     // (CM_DIAG_SPLIT 0: one full diagonal box)
       if (pol)
         tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
       else
@@ -530,7 +554,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
 
 template <int NT, bool BULK, bool RAND>
 __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap,
-                                                                    const __grid_constant__ CUtensorMap tmap_d) {
+                                                                    const __grid_constant__ DiagMaps dmaps) {
   extern __shared__ __align__(1024) unsigned char k1raw[];
   unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
   k1_setup<NT, BULK, RAND>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
@@ -538,7 +562,7 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
   __shared__ int sq[32][8];
   const K1Plain hk{p.sn, p.n_theta, p.th0, p.cs, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
                    (int)((gridDim.x * blockDim.x) >> 5)};
-  k1_body<NT, BULK, RAND>(p, &tmap, &tmap_d, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
+  k1_body<NT, BULK, RAND>(p, &tmap, &dmaps, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
 }
 
 
@@ -1222,7 +1246,7 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
 template <int NT, bool BULK, bool RAND, typename ET>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
                                                                          const __grid_constant__ CUtensorMap tmap,
-                                                                         const __grid_constant__ CUtensorMap tmap_d) {
+                                                                         const __grid_constant__ DiagMaps dmaps) {
   constexpr int KF1 = k1_warps(NT);
   extern __shared__ __align__(1024) unsigned char fraw[];
   unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
@@ -1246,7 +1270,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   if (warp < KF1) {                                                 // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl};
-    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &tmap_d, k1smem, warp, sq[warp], hk);
+    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, warp, sq[warp], hk);
     return;
   }
   // ---- scan (K2) warps
