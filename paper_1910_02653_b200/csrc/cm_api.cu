@@ -371,7 +371,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   sp.o_drec = g->o_drec;
   sp.n_slot = g->n_slot;
   sp.o_qinfo = g->o_qinfo;
-  sp.prefetch = env_flag("CM_PREFETCH", 1);
+  // fused kernel: bit 0 = L2-prefetch a task's blocks when it starts, bit 1 = the next task's
+  // (claimed one ahead) when its unit is already filled; the two-kernel scan: nonzero = on
+  sp.prefetch = env_flag("CM_PREFETCH", 1);   // measured: 3 -> +8.5 KB/S* DRAM reads, same speed
   sp.cs = cs;
   sp.G = G;
   sp.brow = cm2::brow_off(n, m32);

@@ -1313,12 +1313,8 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     uint32_t* ws = fp.ring + (int64_t)slot * fp.slot_words;
     int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
     warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
-    scan_prefetch(sp, ws, ncand, g, (int64_t)batch * 32 + lane);
-#ifndef CM_NO_NEXT_PREFETCH
-    if ((int64_t)t_next < fp.total_tasks) {
-#else
-    if (false) {
-#endif
+    if (sp.prefetch & 1) scan_prefetch(sp, ws, ncand, g, (int64_t)batch * 32 + lane);
+    if ((sp.prefetch & 2) && (int64_t)t_next < fp.total_tasks) {
       const Task e = decode(t_next);
       bool ready = false;
       if (lane == 0) ready = ld_acquire(fp.ctl + 1 + e.slot) >= (uint32_t)(32 * e.k + e.ns);
