@@ -387,6 +387,22 @@ def main():
                       "each call on the launching stream)",
             "alg_bytes_per_launch": alg_bytes, "ms_per_launch": path_ms, "kernels": kernels,
             "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    if a.samples:
+        # randomized rounding is bound by integer ALU work (Philox), not HBM.  Algorithmic
+        # integer ops: per stored element and Philox block (4 samples) 10 rounds x (2 mulhilo =
+        # 4 multiplies, 4 xors, 2 key adds) = 100, plus per sample shift, convert, scale and
+        # compare (4); so 100 / 4 + 4 = 29 per element and candidate.  Peak: the
+        # guide's pipe rates (ALU and FMA pipes each one warp instruction per 2 cycles per SMSP,
+        # 4 SMSPs) x 32 lanes x 148 SMs x the 1965 MHz max SM clock.
+        ops = 29.0 * (g.n * (g.n - 1) // 2) * batch * n_theta
+        clk = (clocks or {}).get("sm_mhz") or 1965.0
+        peak_ops = 148 * 4 * 32 * clk * 1e6
+        ach = ops / (path_ms / 1000.0)
+        roof = {"bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (int32 lane ops)",
+                "frac": ach / peak_ops, "traffic": None, "kernel": roof["kernel"], "ms_per_launch": path_ms,
+                "kernels": kernels, "alg_ops_per_launch": ops,
+                "peak_source": "derived: 148 SMs x 4 SMSPs x 32 lanes x SM clock (B300_MICROARCH pipe rates: ALU and "
+                               "FMA pipes each 1 warp-instr / 2 cycles / SMSP)"}
     cpu = None
     if not a.no_cpu_baseline and world == 1 and not a.samples:
         cpu = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
