@@ -153,9 +153,9 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
       k0 += 0x9E3779B9u;
       k1 += 0xBB67AE85u;
     }
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;             // one IMAD.WIDE.U32 each
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0);
   }
   return c;
 }
@@ -494,8 +494,12 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
             const uint4 o = philox4x32_10(make_uint4((uint32_t)(32 * w + q), (uint32_t)rq, sg, (uint32_t)(p.th0 >> 2)),
                                           p.key0, p.key1);
             const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+            // u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < ceil(x 2^24): the scaling is exact in fp32,
+            // t is clamped to [0, 2^24] (x > 1 or inf: always; x <= 0: never) and NaN converts to 0
+            const float xs = x[q] * 16777216.0f;
+            const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
 #pragma unroll
-            for (int j = 0; j < NT; ++j) rw[j] |= uniform24(ow[j]) < x[q] ? (1u << q) : 0u;
+            for (int j = 0; j < NT; ++j) rw[j] |= (ow[j] >> 8) < t ? (1u << q) : 0u;
           }
 #pragma unroll
           for (int j = 0; j < NT; ++j) word[j] = rw[j] & rmask;
