@@ -447,3 +447,38 @@ def test_int32_state_near_limit(layout):
     assert int(g.mem.sum()) // 3 < 2 ** 31
     x = gen_sstar(g, "mix", 19, 0, 8)
     compare(g, x, [0.5, 0.2], [B.p_floor(g), B.p_live(g)], masks=True, layout=layout)
+
+
+def test_bench_launch_configuration_sampled():
+    """The exact launch bench.py times: ResNet-50 (n=353), 125 000 device-generated G1 S* in the
+    dense layout with 128-byte rows (ld = 384), theta 0.5, 16 budgets, one fused launch;
+    sampled candidates against the oracle, every per-budget key against the GPU's own
+    per-candidate outputs."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    g = G.resnet50()
+    N = 125000
+    dg = DeviceGenerator(g, "g1", 20250101, layout="dense", ld=384)
+    buf = torch.empty(dg.shape(N), dtype=torch.float32, device="cuda")
+    dg.fill(buf, 0)
+    graph = cm.Graph.from_workload(g)
+    budgets = B.geometric_grid(g, 16)
+    out = cm.round_and_evaluate(graph, buf, torch.tensor([0.5], device="cuda"), torch.tensor(budgets, device="cuda"))
+    torch.cuda.synchronize()
+    assert cm.debug_last_launches() == 1
+    peak, cost = out["peak"].cpu().numpy(), out["cost"].cpu().numpy()
+    del buf
+    inst = Instance.from_graph(g)
+    rng = np.random.default_rng(7)
+    for s in sorted(set(rng.integers(0, N, 14).tolist()) | {0, 31, 32, N - 1}):
+        o = evaluate(inst, gen_sstar(g, "g1", 20250101, s, 1)[0], 0.5)
+        assert (peak[s], cost[s]) == (o["peak"], o["cost"]), s
+    bits = out["idx_bits"]
+    for b, key in enumerate(out["best_key"].cpu().numpy()):
+        feas = np.nonzero(peak <= budgets[b])[0]
+        if len(feas) == 0:
+            assert key == KEY_NONE
+            continue
+        c = cost[feas].min()
+        assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, feas[cost[feas] == c].min())
