@@ -276,6 +276,8 @@ def main():
         if i is not None:
             k_end[i].record(stream)
         global_best(key)
+        if bkey is not None:
+            global_best(bkey)
 
     for _ in range(max(a.warmup, 3)):
         step()

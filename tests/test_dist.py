@@ -115,3 +115,73 @@ def test_shard_ranges_cover():
             assert rs[0][0] == 0 and rs[-1][1] == N
             assert all(rs[i][1] == rs[i + 1][0] for i in range(P - 1))
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def _mask_worker(rank, world, port, n_sstar, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import importlib.util
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        spec = importlib.util.spec_from_file_location("cm_dist", os.path.join(root, "paper_1910_02653_b200", "dist.py"))
+        D = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(D)
+        import numpy as np
+        from oracle import Instance, evaluate, masks_u64
+        from workloads import budgets as B
+        from workloads import graphs as G
+        from workloads.sstar import gen_sstar
+        g = G.random_training(6, 0.2, 3)
+        inst = Instance.from_graph(g)
+        budgets = list(B.geometric_grid(g, 6))
+        lo, hi = D.shard_range(n_sstar, rank, world)
+        idx_bits = max(1, (n_sstar - 1).bit_length())
+        peaks, costs, rm, sm = [], [], [], []
+        for s in range(lo, hi):
+            o = evaluate(inst, gen_sstar(g, "mix", 17, s, 1)[0], 0.5, keep=True)
+            peaks.append(o["peak"])
+            costs.append(o["cost"])
+            rm.append(masks_u64(inst, o["R"]).view(np.int64))
+            sm.append(masks_u64(inst, o["S"]).view(np.int64))
+        keys = torch.tensor(_keys_for(peaks, costs, budgets, lo, idx_bits), dtype=torch.int64)
+        D.global_best(keys)
+        got = D.gather_winner_masks(keys, idx_bits, lo, torch.from_numpy(np.stack(rm)), torch.from_numpy(np.stack(sm)))
+        out_q.put((rank, keys.tolist(), got.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_winner_masks_two_ranks():
+    """Every rank ends with the R / S masks of every budget's global winner."""
+    import numpy as np
+    from oracle import Instance, evaluate, masks_u64
+    from workloads import graphs as G
+    from workloads.sstar import gen_sstar
+    n_sstar = 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mask_worker, args=(r, 2, port, n_sstar, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = G.random_training(6, 0.2, 3)
+    inst = Instance.from_graph(g)
+    idx_bits = max(1, (n_sstar - 1).bit_length())
+    (_, keys, m0), (_, keys1, m1) = res
+    assert keys == keys1 and np.array_equal(m0, m1)
+    seen = 0
+    for b, k in enumerate(keys):
+        if k == KEY_NONE:
+            assert not m0[b].any()
+            continue
+        i = k & ((1 << idx_bits) - 1)
+        o = evaluate(inst, gen_sstar(g, "mix", 17, i, 1)[0], 0.5, keep=True)
+        assert np.array_equal(m0[b, 0].view(np.uint64), masks_u64(inst, o["R"]))
+        assert np.array_equal(m0[b, 1].view(np.uint64), masks_u64(inst, o["S"]))
+        seen += 1
+    assert seen >= 2
