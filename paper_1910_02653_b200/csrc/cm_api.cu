@@ -445,6 +445,18 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         fp.n_units = (int32_t)units;
         fp.tpu = G * nt;
         fp.total_tasks = total_tasks;
+        {  // ~64 blocks of rounding work per ticket: 8 S* at n = 89, 1 at n = 353
+          const int gr = n >= 2 ? (n - 2) / 32 + 1 : 1;
+          const int blocks = gr * (gr + 1) / 2;
+          int c = 1;
+          while (c < 8 && 2 * c * blocks <= 64) c *= 2;
+          fp.claim = env_flag("CM_CLAIM", c);
+          if (fp.claim < 1 || fp.claim > 32 || (fp.claim & (fp.claim - 1))) fp.claim = c;
+          // scan tasks per consumer ticket (tuning; 1: measured a whole VGG16 unit per ticket
+          // at 121 vs 153 M cand/s -- the unit's three tasks then run one after another)
+          fp.task_claim = env_flag("CM_TASK_CLAIM", 1);
+          if (fp.task_claim < 1 || fp.tpu % fp.task_claim) fp.task_claim = 1;
+        }
         std::lock_guard<std::mutex> lock(g->mu);
         e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
         if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");

@@ -1192,6 +1192,8 @@ struct FusedParams {
   int32_t n_units;
   int32_t tpu;                // tasks of a full unit: G * n_theta
   int64_t total_tasks;
+  int32_t claim;              // S* per producer ticket (power of two <= 32)
+  int32_t task_claim;         // scan tasks per consumer ticket (divides tpu)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -1216,22 +1218,29 @@ struct K1Ring {
   int64_t slot_words;
   int32_t n_slots, n_theta, cs;
   uint32_t* ctl;
-  // S* tickets (in order across all K1 warps; a CTA that starts late simply takes later ones)
+  int32_t claim;              // S* per ticket (a power of two <= 32: a claim never straddles a unit)
+  int32_t s_count;
+  // S* tickets (in order across all K1 warps; a CTA that starts late simply takes later ones).
+  // Small graphs take several consecutive S* per ticket, so the fence and the count are paid
+  // once per claim rather than once per S*.
   __device__ __forceinline__ int first() const {
     uint32_t t = 0;
     if ((threadIdx.x & 31) == 0) t = atomicAdd(ctl + 1 + 3 * n_slots, 1u);
-    return (int)__shfl_sync(FULL, t, 0);
+    return (int)__shfl_sync(FULL, t, 0) * claim;
   }
-  __device__ __forceinline__ int next(int) const { return first(); }
+  __device__ __forceinline__ int next(int s) const { return ((s + 1) & (claim - 1)) ? s + 1 : first(); }
   __device__ __forceinline__ uint32_t* begin(int s) const {
     const int u = s >> 5, slot = u % n_slots, k = u / n_slots;
-    if (k > 0) warp_wait_geq(ctl + 1 + 2 * n_slots + slot, (uint32_t)k);
+    if (k > 0 && (s & (claim - 1)) == 0) warp_wait_geq(ctl + 1 + 2 * n_slots + slot, (uint32_t)k);
     return ring + (int64_t)slot * slot_words + (int64_t)(s & 31) * n_theta * cs;
   }
   __device__ __forceinline__ void end(int s) const {
+    if ((s & (claim - 1)) != claim - 1 && s != s_count - 1) return;   // not the claim's last S*
+#ifndef CM_EXP_NOFENCE
     __threadfence();                                                // this lane's blocks, then the count
+#endif
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) atomicAdd(ctl + 1 + (s >> 5) % n_slots, 1u);
+    if ((threadIdx.x & 31) == 0) atomicAdd(ctl + 1 + (s >> 5) % n_slots, (uint32_t)((s & (claim - 1)) + 1));
   }
 };
 
@@ -1273,7 +1282,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
 
   if (warp < KF1) {                                                 // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
-    const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl};
+    const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
     k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, warp, sq[warp], hk);
     return;
   }
@@ -1307,34 +1316,47 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     d.k = d.u / R;
     return d;
   };
+  // A ticket covers tc consecutive tasks (tc divides tpu, so a claim stays inside one unit):
+  // small graphs take a whole unit per ticket and pay the fence and the count once per unit.
+  const uint32_t tc = (uint32_t)fp.task_claim;
   uint32_t t = claim();
-  while ((int64_t)t < fp.total_tasks) {
+  while ((int64_t)t * tc < fp.total_tasks) {
     const uint32_t t_next = claim();
-    const Task d = decode(t);
-    const int u = d.u, g = d.g, batch = d.batch, slot = d.slot, k = d.k, ns = d.ns;
-    const int64_t ncand = d.ncand;
+    const uint32_t t0 = t * tc;
+    const Task d0 = decode(t0);
+    const int u = d0.u, slot = d0.slot, k = d0.k, ns = d0.ns;
+    const int64_t ncand = d0.ncand;
     const int nb = (int)((ncand + 31) / 32);
+    const uint32_t tasks_u = (uint32_t)(G * nb);
     uint32_t* ws = fp.ring + (int64_t)slot * fp.slot_words;
     int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
     warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
-    if (sp.prefetch & 1) scan_prefetch(sp, ws, ncand, g, (int64_t)batch * 32 + lane);
-    if ((sp.prefetch & 2) && (int64_t)t_next < fp.total_tasks) {
-      const Task e = decode(t_next);
-      bool ready = false;
-      if (lane == 0) ready = ld_acquire(fp.ctl + 1 + e.slot) >= (uint32_t)(32 * e.k + e.ns);
-      if (__shfl_sync(FULL, ready, 0))
-        scan_prefetch(sp, fp.ring + (int64_t)e.slot * fp.slot_words, e.ncand, e.g, (int64_t)e.batch * 32 + lane);
-    }
+    uint32_t cnt = 0;
+    for (uint32_t j = 0; j < tc; ++j) {
+      const uint32_t tt = t0 + j;
+      if ((int64_t)tt >= fp.total_tasks) break;                     // the last unit may be short
+      const Task d = decode(tt);
+      if (sp.prefetch & 1) scan_prefetch(sp, ws, ncand, d.g, (int64_t)d.batch * 32 + lane);
+      if ((sp.prefetch & 2) && tc == 1 && (int64_t)t_next < fp.total_tasks) {
+        const Task e = decode(t_next);
+        bool ready = false;
+        if (lane == 0) ready = ld_acquire(fp.ctl + 1 + e.slot) >= (uint32_t)(32 * e.k + e.ns);
+        if (__shfl_sync(FULL, ready, 0))
+          scan_prefetch(sp, fp.ring + (int64_t)e.slot * fp.slot_words, e.ncand, e.g, (int64_t)e.batch * 32 + lane);
+      }
 #ifndef CM_EXP_NOSCAN
-    scan_task<ET, true>(sp, x, g, (int64_t)batch * 32, ws, ncand, part, (int64_t)u * unit_cands);
+      scan_task<ET, true>(sp, x, d.g, (int64_t)d.batch * 32, ws, ncand, part, (int64_t)u * unit_cands);
 #endif
+      ++cnt;
+    }
+#ifndef CM_EXP_NOFENCE
     __threadfence();                                                // reads done, partials visible
+#endif
     __syncwarp();
-    const uint32_t tasks_u = (uint32_t)(G * nb);
     uint32_t old = 0;
-    if (lane == 0) old = atomicAdd(fp.ctl + 1 + R + slot, 1u);
+    if (lane == 0) old = atomicAdd(fp.ctl + 1 + R + slot, cnt);
     old = __shfl_sync(FULL, old, 0);
-    if (old + 1 == (uint32_t)fp.tpu * (uint32_t)k + tasks_u) {       // last task of unit u: reduce it
+    if (old + cnt == (uint32_t)fp.tpu * (uint32_t)k + tasks_u) {     // last task of unit u: reduce it
       __threadfence();
       for (int64_t c = lane; c < ncand; c += 32) reduce_one(fp.qp, part, c, (int64_t)u * unit_cands);
       __threadfence();                                              // partials read: release the slot
