@@ -796,7 +796,11 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
     rec1 = nrec[k - 1];                                             // k = 0: the sentinel record
     const int64_t Ck = C[k];
     const uint32_t sn = sn1;
-    sn1 = u == 0 ? nquad.w : u == 1 ? quad.x : u == 2 ? quad.y : quad.z;   // Sn_{k-1}
+    {  // Sn_{k-1}: component u-1 of the quad, or the next quad's last word (branch-free selects)
+      const uint32_t c01 = (u & 2) ? quad.y : quad.x;              // u = 2 -> y, u = 1 -> x
+      const uint32_t c = u == 3 ? quad.z : c01;
+      sn1 = u == 0 ? nquad.w : c;
+    }
     const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;             // A'_k, complete
     const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);     // S_t from S_{t+1} and row 32g
     const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
