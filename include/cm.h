@@ -144,6 +144,10 @@ int32_t cm_debug_trace(float* out, int32_t max_values);
 /* Debug aid: the number of kernels the calling thread's last cm_round_and_evaluate launched
  * (1 on the fused persistent path; per chunk ceil(n_theta/4) + 2 on the two-kernel pipeline). */
 int32_t cm_debug_last_launches(void);
+/* Debug aid: with CM_TRACE=2, the fused kernel records per CTA {start, rounding warps done,
+ * ~(first wait for unit 0 satisfied), scan warps done} in %globaltimer ns; after the call
+ * completed this copies up to max_values of them and returns the count (0 if none). */
+int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values);
 
 /*
  * Execution plans for chosen schedules.  Algorithm 1 "Generate execution

@@ -22,7 +22,7 @@ CM_ROUND_THRESHOLD = 0
 CM_ROUND_RANDOMIZED = 1
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
-           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
+           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
            "cm_policy_checkpoints", "cm_policy_sstar", "cm_policy_last_error",
            "cm_last_error")
 
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_debug_trace.restype = ctypes.c_int32
     lib.cm_debug_last_launches.argtypes = []
     lib.cm_debug_last_launches.restype = ctypes.c_int32
+    lib.cm_debug_cta_trace.argtypes = [P, ctypes.c_int32]
+    lib.cm_debug_cta_trace.restype = ctypes.c_int32
     lib.cm_key_idx_bits.argtypes = [ctypes.c_int64]
     lib.cm_key_idx_bits.restype = ctypes.c_int32
     lib.cm_decode_key.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),

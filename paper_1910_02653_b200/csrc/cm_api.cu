@@ -140,6 +140,8 @@ struct Trace {
   int used = 0;
 };
 Trace g_trace;
+uint64_t* g_cta_trace = nullptr;       // CM_TRACE=2: per-CTA timestamps of the last fused launch
+int32_t g_cta_trace_n = 0;
 thread_local int32_t g_launches = 0;   // kernels launched by this thread's last cm_round_and_evaluate
 bool trace_enabled() {
   const char* e = std::getenv("CM_TRACE");
@@ -404,8 +406,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
-    const int64_t total_tasks = (units - 1) * (int64_t)G * nt +
-                                (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
+    // scan-task tickets: unit-major (CM_WIN=0) or windows of CM_WIN units, group-major inside
+    const int64_t win = std::max<int64_t>(0, std::min<int64_t>(env_flag("CM_WIN", 32), 256));
+    const int64_t total_tasks = win > 0 ? ((units + win - 1) / win) * win * (int64_t)G * nt
+                                        : (units - 1) * (int64_t)G * nt +
+                                              (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
     int64_t ring_max = env_flag("CM_RING", 768);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
     int64_t R = std::min<int64_t>(ring_max, units);
     auto ctl_bytes = [](int64_t r) { return (4 * (2 + 3 * r) + 255) & ~int64_t(255); };
@@ -445,6 +450,14 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         fp.n_units = (int32_t)units;
         fp.tpu = G * nt;
         fp.total_tasks = total_tasks;
+        fp.win_units = (int32_t)win;
+        fp.trace = nullptr;
+        if (env_flag("CM_TRACE", 0) == 2) {
+          if (!g_cta_trace) cudaMalloc(&g_cta_trace, 4 * sizeof(uint64_t) * 1024);
+          g_cta_trace_n = 4 * g->sm_count;
+          if (g_cta_trace) cudaMemsetAsync(g_cta_trace, 0, 4 * sizeof(uint64_t) * g->sm_count, st);
+          fp.trace = g_cta_trace;
+        }
         {  // ~64 blocks of rounding work per ticket: 8 S* at n = 89, 1 at n = 353
           const int gr = n >= 2 ? (n - 2) / 32 + 1 : 1;
           const int blocks = gr * (gr + 1) / 2;
@@ -455,7 +468,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           // scan tasks per consumer ticket (tuning; 1: measured a whole VGG16 unit per ticket
           // at 121 vs 153 M cand/s -- the unit's three tasks then run one after another)
           fp.task_claim = env_flag("CM_TASK_CLAIM", 1);
-          if (fp.task_claim < 1 || fp.tpu % fp.task_claim) fp.task_claim = 1;
+          if (fp.task_claim < 1 || fp.tpu % fp.task_claim || win > 0) fp.task_claim = 1;
         }
         std::lock_guard<std::mutex> lock(g->mu);
         e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
@@ -858,6 +871,13 @@ int32_t cm_debug_trace(float* out, int32_t max_values) {
 }
 
 int32_t cm_debug_last_launches(void) { return g_launches; }
+
+int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values) {
+  if (!g_cta_trace || !out) return 0;
+  const int32_t m = std::min(max_values, g_cta_trace_n);
+  if (cudaMemcpy(out, g_cta_trace, sizeof(uint64_t) * (size_t)m, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return m;
+}
 
 cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const uint8_t* k_sets, float* sstar,
                           int64_t ld, cm_stream stream) {

@@ -1198,7 +1198,15 @@ struct FusedParams {
   int64_t total_tasks;
   int32_t claim;              // S* per producer ticket (power of two <= 32)
   int32_t task_claim;         // scan tasks per consumer ticket (divides tpu)
+  int32_t win_units;          // ticket windows (units), 0: unit-major order
+  uint64_t* trace;            // debug (CM_TRACE=2): per CTA {start, K1 end, ~first unit-0 task, K2 end} ns
 };
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -1283,11 +1291,13 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (fp.trace && threadIdx.x == 0) fp.trace[4 * blockIdx.x] = globaltimer();
 
   if (warp < KF1) {                                                 // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
     k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, warp, sq[warp], hk);
+    if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 1), globaltimer());
     return;
   }
   // ---- scan (K2) warps
@@ -1306,16 +1316,33 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   struct Task {
     int u, g, batch, slot, k, ns;
     int64_t ncand;
+    bool valid;
   };
+  // Ticket order.  win_units == 0: unit by unit, big groups first inside a unit.  Otherwise
+  // windows of win_units units, each ordered (group descending, unit, batch), so the longest
+  // tasks of the batch's last units are claimed early and the launch does not end on one
+  // long walk (tickets of a short last window / unit that name no task are skipped).
   auto decode = [&](uint32_t t) {
     Task d;
-    d.u = (int)(t / (uint32_t)fp.tpu);
-    const int sub = (int)(t - (uint32_t)d.u * (uint32_t)fp.tpu);
-    d.ns = min(32, fp.n_sstar - 32 * d.u);                          // S* of this unit
+    int sub;
+    if (fp.win_units == 0) {
+      d.u = (int)(t / (uint32_t)fp.tpu);
+      sub = (int)(t - (uint32_t)d.u * (uint32_t)fp.tpu);
+    } else {
+      const uint32_t per_win = (uint32_t)fp.win_units * (uint32_t)fp.tpu;
+      const uint32_t w = t / per_win, r = t - w * per_win;
+      const uint32_t per_g = (uint32_t)fp.win_units * (uint32_t)fp.n_theta;   // full-unit batches
+      const uint32_t gi = r / per_g, rr = r - gi * per_g;
+      d.u = (int)(w * (uint32_t)fp.win_units + rr / (uint32_t)fp.n_theta);
+      sub = (int)(gi * (uint32_t)fp.n_theta + rr % (uint32_t)fp.n_theta);
+    }
+    d.valid = d.u < fp.n_units;
+    d.ns = d.valid ? min(32, fp.n_sstar - 32 * d.u) : 0;            // S* of this unit
     d.ncand = (int64_t)d.ns * fp.n_theta;
-    const int nb = (int)((d.ncand + 31) / 32);                      // candidate batches of the unit
+    const int nb = fp.win_units == 0 ? (int)((d.ncand + 31) / 32) : fp.n_theta;   // batches per group slot
     d.g = G - 1 - sub / nb;                                         // big groups first
     d.batch = sub % nb;
+    d.valid = d.valid && (int64_t)d.batch * 32 < d.ncand;
     d.slot = d.u % R;
     d.k = d.u / R;
     return d;
@@ -1328,6 +1355,10 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     const uint32_t t_next = claim();
     const uint32_t t0 = t * tc;
     const Task d0 = decode(t0);
+    if (!d0.valid) {                                                // a ticket that names no task
+      t = t_next;
+      continue;
+    }
     const int u = d0.u, slot = d0.slot, k = d0.k, ns = d0.ns;
     const int64_t ncand = d0.ncand;
     const int nb = (int)((ncand + 31) / 32);
@@ -1335,6 +1366,8 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     uint32_t* ws = fp.ring + (int64_t)slot * fp.slot_words;
     int64_t* part = reinterpret_cast<int64_t*>(ws + unit_cands * sp.cs);
     warp_wait_geq(fp.ctl + 1 + slot, (uint32_t)(32 * k + ns));
+    if (fp.trace && lane == 0 && u == 0)                            // first unit ready (any warp)
+      atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 2), ~globaltimer());   // min
     uint32_t cnt = 0;
     for (uint32_t j = 0; j < tc; ++j) {
       const uint32_t tt = t0 + j;
@@ -1371,6 +1404,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   }
   x.A.wait_st();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 3), globaltimer());
   asm volatile("bar.sync 1, %0;" :: "r"(32 * kFusedScanWarps) : "memory");   // the scan warps only
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == KF1)
