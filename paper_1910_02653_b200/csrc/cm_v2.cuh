@@ -605,7 +605,9 @@ struct ScanParams {
 // live in Tensor Memory -- lane = TMEM lane (this warp's 32-lane quarter), slot = TMEM
 // column, accessed with tcgen05.ld/st.32x32b (one column, all 32 lanes, uniform address)
 // -- and slots >= tmc spill to shared memory.  A load after a store of the same column is
-// ordered by tcgen05.wait::st (the walk tracks pending stores).
+// ordered by tcgen05.wait::st (the walk tracks pending stores).  The TMEM asm carries no
+// "memory" clobber: TMEM is not memory, volatile asm keeps the ld / st / wait order, and
+// register operands order the uses -- so shared-memory work (E) may move across them.
 template <bool TM>
 struct AView {
   uint32_t* sm;
@@ -619,32 +621,32 @@ struct AView {
   __device__ __forceinline__ uint32_t ld_async(int s) const {   // TMEM: value valid after wait_ld()
     uint32_t v;
     if (in_tmem<MODE>(s))
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)s) : "memory");
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr + (uint32_t)s));
     else
       v = sm[32 * (s - tmc) + lane];
     return v;
   }
   __device__ __forceinline__ void wait_ld(uint32_t& v) const {
-    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) :: "memory");
+    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v));
   }
   __device__ __forceinline__ void wait_ld3(uint32_t& v0, uint32_t& v1, uint32_t& v2) const {
-    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v0), "+r"(v1), "+r"(v2) :: "memory");
+    if (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v0), "+r"(v1), "+r"(v2));
   }
   template <int MODE>
   __device__ __forceinline__ void st(int s, uint32_t v) const {
     if (in_tmem<MODE>(s))
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)s), "r"(v) : "memory");
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr + (uint32_t)s), "r"(v));
     else
       sm[32 * (s - tmc) + lane] = v;
   }
   __device__ __forceinline__ void wait_st() const {
-    if (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if (TM) asm volatile("tcgen05.wait::st.sync.aligned;");
   }
   // slots s..s+3, all in TMEM (TM, s + 3 < tmc)
   __device__ __forceinline__ void st4(int s, uint4 v) const {
     if (TM)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
-                   :: "r"(taddr + (uint32_t)s), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+                   :: "r"(taddr + (uint32_t)s), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
   }
 };
 
