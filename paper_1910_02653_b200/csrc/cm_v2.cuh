@@ -1,24 +1,22 @@
 // cm_v2.cuh -- stage-sliced sm_100a kernels for Checkmate two-phase rounding (Alg. 2,
 // PAPER.md:389-415) and the Eq. 6-9 memory accounting.
 //
-// "Stage-sliced": a 32-bit word holds one node's bit for 32 consecutive stages.  A lane
-// owns a group g of 32 stages (rows 32g..32g+31, 0-based row r = stage t-1) of one
-// candidate, so every bitwise step of the method runs for 32 stages at once and the control
-// flow (a walk over the graph) is identical in all lanes: no per-stage divergence, however
-// recomputation is distributed over the stages.
+// "Stage-sliced": a 32-bit word holds one node's bit for 32 consecutive stages (group g =
+// rows 32g..32g+31, 0-based row r = stage t-1), so every bitwise step of the method runs for
+// 32 stages at once, and a warp takes lane = candidate with the same group in all lanes: the
+// control flow (a walk over the graph) is uniform however recomputation is distributed.
 //
-// K1 round_pack_kernel (HBM-bound).  Task = (S*, row group g).  For each 32x32 block
-//   (w = 0..g) lane l loads row r = 32g+l+1 with 16-byte streaming loads, compares > theta
-//   (a1: strict, fp32, NaN -> 0) into a row word, and a 5-step shuffle
-//   transpose turns the 32 row words into column words
+// K1 body (k1_body; HBM-bound), per S*: for each 32x32 block (g, w <= g) -- rows 32g+1+l,
+//   nodes 32w.. -- lane l reads its row from a TMA-staged tile, packs x > theta (a1,
+//   strict, fp32, NaN -> 0) into its row word, adds the row's checkpoint mass
+//   (the Eq. 6 sum) from 4-bit tables, and a 5-step shuffle transpose gives the column words
 //       Sn_g[i]  bit b = S_{row 32g+b+1, node i} = S_{t+1}   for stage t = 32g+b+1,
 //   i.e. the NEXT stage's checkpoint bits (S_{n+1} = 0).  The current stage's
-//   bits follow from them: Sw_g = (Sn_g << 1) | (Sn_{g-1} >> 31).  One S* read serves every
-//   threshold.
+//   bits follow from them and row 32g's word (brow).  One S* read serves up to 4 thresholds
+//   (or 4 random samples, RAND: Philox4x32-10, R1).
 //
-// K2 scan_kernel (ALU / latency-bound).  One warp evaluates cpw candidates, lanes =
-//   (candidate, group).  A single pass over nodes k = n-1 .. 0 (reverse topological order,
-//   the paper's right-to-left repair scan), push form:
+// K2 task (scan_task; latency / ALU-bound), per (group g, 32 candidates): one pass over nodes
+//   k = nk-1 .. 0 (reverse topological order, the paper's right-to-left scan):
 //     R_k   = ((Sn_k | Acc_k) & ~Sw_k) | diag_k      a2 seed S_{t+1} & ~S_t, e_t; a3 closure
 //             Acc_k = OR of R_j over the users j > k (all visited before k)
 //     FREE  i in DEPS(k): R_k & ~Sn_i & ~Acc_i       Eq. 9: k computed, i not kept, no later user
@@ -27,11 +25,23 @@
 //   Memory: with D = U_{t,k} - U_{t,end} run backwards and MX = max over computes of D,
 //   only E = MX - D matters:  frees:  E -= M_i ;  compute of k:  E = max(E, 0) + M_k.
 //   Then peak_t = U_{t,0} + E_t (the max over k is reached at a compute,
-//   DESIGN.md Q9), with U_{t,0} = ovh + mass_t (Eq. 6) from K1.  The per-stage int64 E sits
-//   in shared memory and is touched only at set bits (events).
+//   DESIGN.md Q9), with U_{t,0} = ovh + mass_t (Eq. 6) from K1.
 //
-// Layout of one candidate's column array in the workspace: group g holds nodes 0..32g+31 at
-// word offset grp_off(g) = 16 g (g+1) (16-byte aligned).
+// Reduce (reduce_one): per candidate max / sum over groups, the a7 per-budget keys and the
+//   optional max-batch keys.
+//
+// Kernels: fused_kernel (one persistent launch; K1 warps and K2 warps per CTA, hand-off through
+// a ring in global memory -- the default path), or round_tma_kernel + scan_kernel +
+// reduce_kernel on two streams (the two-kernel pipeline: > 4 thresholds, randomized rounding
+// with the int64 state, or no shared-memory / TMEM fit).
+//
+// Build-time switches: tuning (CM_K1_WARPS1, CM_K1_STAGES1, CM_K1_REGS1, CM_KF2,
+// CM_DIAG_BULK, CM_DIAG_SPLIT) and timing experiments that break the results on purpose
+// (CM_EXP_L2INPUT: every S* read from 64 L2-resident ones; CM_EXP_NOSCAN: no walks;
+// CM_EXP_NOFENCE: no hand-off fences) -- tools/build_variant.py builds them into tune/.
+//
+// Layout of one candidate block: group g's Sn columns (nodes 0..32g+31) at word offset
+// grp_off(g) = 16 g (g+1) (whole 128-byte lines), then the masses, then brow.
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
