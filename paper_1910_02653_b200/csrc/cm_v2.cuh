@@ -531,6 +531,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
           if (lane == 31 && g + 1 < G) oj[brow_at] = word[j];
           oj[grp_off(g) + node] = transpose(word[j]);               // node 32w+lane's column: bit b = row 32g+1+b
         }
+#ifndef CM_EXP_NOMASS                                               // timing experiment: no masses
         if (scaled32) {                                             // scaled masses fit int32
           const unsigned char* tb = reinterpret_cast<const unsigned char*>(nib32 + 128 * w);
 #pragma unroll
@@ -553,6 +554,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
             mass[j] += ms;
           }
         }
+#endif
       }
       if (rq < p.n) {
 #pragma unroll
