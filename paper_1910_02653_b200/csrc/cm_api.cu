@@ -406,15 +406,19 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
-    // scan-task tickets: unit-major (CM_WIN=0) or windows of CM_WIN units, group-major inside
-    const int64_t win = std::max<int64_t>(0, std::min<int64_t>(env_flag("CM_WIN", 32), 256));
-    const int64_t total_tasks = win > 0 ? ((units + win - 1) / win) * win * (int64_t)G * nt
-                                        : (units - 1) * (int64_t)G * nt +
-                                              (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
+    // scan-task tickets: unit-major (default) or windows of CM_WIN units, group-major inside
+    // (tuning; measured no gain).  Windows reorder tickets against unit order, so a window's
+    // slot predecessors must lie two windows back (W <= R / 2) or a warp blocked on one
+    // window task can hold the ticket that would free its slot: clamped below.
+    int64_t win = std::max<int64_t>(0, std::min<int64_t>(env_flag("CM_WIN", 0), 256));
     int64_t ring_max = env_flag("CM_RING", 768);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
     int64_t R = std::min<int64_t>(ring_max, units);
     auto ctl_bytes = [](int64_t r) { return (4 * (2 + 3 * r) + 255) & ~int64_t(255); };
     while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
+    if (R < units) win = std::min<int64_t>(win, R / 2);             // no slot reuse: any order is safe
+    const int64_t total_tasks = win > 0 ? ((units + win - 1) / win) * win * (int64_t)G * nt
+                                        : (units - 1) * (int64_t)G * nt +
+                                              (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
     if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= ws_bytes &&
         total_tasks < (int64_t(1) << 31)) {
       const void* fn = fused_fn(nt, bulk, rnd, g->scan32);

@@ -291,14 +291,17 @@ def env_var():
             os.environ[k] = v
 
 
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("win", [0, 16])
 @pytest.mark.parametrize("layout", LAYOUTS)
-def test_fused_ring_wraparound(env_var, layout):
+def test_fused_ring_wraparound(env_var, layout, win):
     """Fused path with a 3-slot ring: 1000 S* = 32 units, every slot reused ~10 times
-    (producer / consumer hand-off, slot release after the in-kernel reduce)."""
+    (producer / consumer hand-off, slot release after the in-kernel reduce); with ticket
+    windows requested (clamped to R / 2 so the hand-off cannot deadlock)."""
     import torch
     import paper_1910_02653_b200 as cm
     from workloads.device_gen import DeviceGenerator
-    env_var(CM_RING=3)
+    env_var(CM_RING=3, CM_WIN=win)
     g = G.resnet50()
     N = 1000
     dg = DeviceGenerator(g, "g1", 77, layout=layout)
