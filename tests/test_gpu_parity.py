@@ -485,3 +485,18 @@ def test_bench_launch_configuration_sampled():
             continue
         c = cost[feas].min()
         assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, feas[cost[feas] == c].min())
+
+
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("ring", [1, 2])
+def test_fused_tiny_ring_small_graph(env_var, ring):
+    """VGG16 (producers claim 8 consecutive S* per ticket) through a 1- or 2-slot ring: every
+    unit waits for its predecessor's release; 700 S* = 22 units, one partial."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    env_var(CM_RING=ring)
+    g = G.vgg16()
+    x = gen_sstar(g, "mix", 29, 0, 700)
+    budgets = B.geometric_grid(g, 6)
+    res, outs = compare(g, x, [0.5], budgets)
+    assert cm.debug_last_launches() == 1
