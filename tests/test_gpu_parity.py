@@ -500,3 +500,15 @@ def test_fused_tiny_ring_small_graph(env_var, ring):
     budgets = B.geometric_grid(g, 6)
     res, outs = compare(g, x, [0.5], budgets)
     assert cm.debug_last_launches() == 1
+
+
+@pytest.mark.parametrize("name", ["random", "vgg16", "resnet50"])
+def test_row_form_kernel(env_var, name):
+    """The row-form fallback (one CTA per S*, used when the stage-sliced layout does not fit
+    shared memory), forced with CM_KERNEL=v1."""
+    import paper_1910_02653_b200 as cm
+    env_var(CM_KERNEL="v1")
+    g = {"random": lambda: G.random_training(18, 0.2, 3), "vgg16": G.vgg16, "resnet50": G.resnet50}[name]()
+    x = gen_sstar(g, "mix", 31, 0, 6)
+    compare(g, x, [0.5, 0.3], B.geometric_grid(g, 5), masks=(name != "resnet50"))
+    assert cm.debug_last_launches() == 1
