@@ -1273,7 +1273,10 @@ struct K1Ring {
 #ifndef CM_KF2
 #define CM_KF2 8
 #endif
-constexpr int kFusedScanWarps = CM_KF2;                            // scan warps per fused CTA
+// scan warps per fused CTA.  Measured: 10 (96 registers, spills) 17.3 vs 18.5 M cand/s for 8;
+// setmaxnreg to rebalance registers needs whole warpgroups (10 scan warps hang), and 12 do
+// not fit in shared memory at n = 353.
+constexpr int kFusedScanWarps = CM_KF2;
 constexpr int kFusedTmemCols = 512 / ((kFusedScanWarps + 3) / 4);  // per scan warp
 __host__ __device__ constexpr int fused_warps(int nt) { return k1_warps(nt) + kFusedScanWarps; }
 // dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
