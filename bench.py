@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--layout", default="dense", choices=["tri4", "dense"])
     ap.add_argument("--ld", type=int, default=None,
                     help="dense row stride in floats (default: n rounded up to 32, i.e. 128-byte rows)")
+    ap.add_argument("--overlap", default="on", choices=["on", "off"],
+                    help="consecutive steps' calls with CM_EVAL_OVERLAP | CM_EVAL_INIT_KEYS on two "
+                         "alternating output sets (a call starts while the previous one drains)")
+    ap.add_argument("--step-events", action="store_true",
+                    help="with --overlap on: also record CUDA events around every call")
     ap.add_argument("--e2e-batch", type=int, default=16384)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -274,32 +279,43 @@ def main():
     gen.fill(sstar, s_base)
     th = torch.tensor(thetas, dtype=torch.float32, device=dev)
     bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
-    key = torch.empty(len(budgets), dtype=torch.int64, device=dev)
-    bkey = torch.empty(len(budgets), dtype=torch.int64, device=dev) if a.max_batch else None
+    overlap = a.overlap == "on"
+    n_sets = 2 if overlap else 1                     # overlapped calls alternate two output sets
+    keys = [torch.empty(len(budgets), dtype=torch.int64, device=dev) for _ in range(n_sets)]
+    bkeys = [torch.empty(len(budgets), dtype=torch.int64, device=dev) if a.max_batch else None
+             for _ in range(n_sets)]
     from workloads.budgets import eq13_cost_limit
     limit = eq13_cost_limit(g) if a.max_batch else None
-    peak = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
-    cost = torch.empty(batch * n_theta, dtype=torch.int64, device=dev)
+    peaks = [torch.empty(batch * n_theta, dtype=torch.int64, device=dev) for _ in range(n_sets)]
+    costs = [torch.empty(batch * n_theta, dtype=torch.int64, device=dev) for _ in range(n_sets)]
+    calls = [0]
+    events = not overlap or a.step_events
     total = world * batch * n_theta
     stream = torch.cuda.current_stream(dev)
     k_start = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
 
     def step(i=None):
-        key.fill_(cm.CM_KEY_NONE)
-        if bkey is not None:
-            bkey.fill_(cm.CM_KEY_NONE)
-        if i is not None:
+        h = calls[0] % n_sets
+        calls[0] += 1
+        key, bkey = keys[h], bkeys[h]
+        if not overlap:
+            key.fill_(cm.CM_KEY_NONE)
+            if bkey is not None:
+                bkey.fill_(cm.CM_KEY_NONE)
+        if i is not None and events:
             k_start[i].record(stream)
         cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
-                              index_base=s_base * n_theta, total_candidates=total, best_key=key, peak=peak,
-                              cost=cost, stream=stream.cuda_stream, samples=a.samples, seed=seed,
-                              cost_limit=limit, best_batch_key=bkey)
-        if i is not None:
+                              index_base=s_base * n_theta, total_candidates=total, best_key=key,
+                              peak=peaks[h], cost=costs[h], stream=stream.cuda_stream, samples=a.samples,
+                              seed=seed, cost_limit=limit, best_batch_key=bkey,
+                              init_keys=overlap, overlap=overlap)
+        if i is not None and events:
             k_end[i].record(stream)
         global_best(key)
         if bkey is not None:
             global_best(bkey)
+        return key
 
     for _ in range(max(a.warmup, 3)):
         step()
@@ -317,19 +333,21 @@ def main():
         dist.barrier()
     t0.record(stream)
     for i in range(a.steps):
-        step(i)
+        last_key = step(i)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     elapsed_ms = t0.elapsed_time(t1)
-    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(k_start, k_end)]))
+    # per-call device time; overlapped calls (no events between them) -> the per-step time
+    kern_ms = (float(np.mean([s.elapsed_time(e) for s, e in zip(k_start, k_end)])) if events
+               else elapsed_ms / a.steps)
     if world > 1:
         t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms, kern_ms = float(t[0]), float(t[1])
-    best = key.cpu().tolist()
+    best = last_key.cpu().tolist()
 
     # ---- e2e through the public API with HOST buffers (rank-local, then the same MIN) ----
     e2e = None
@@ -378,7 +396,8 @@ def main():
     value = cand_per_step * a.steps / (elapsed_ms / 1000.0)
     peak_gbs, peak_src = load_peaks()
     alg_bytes = batch * tri_bytes(g.n) + batch * n_theta * 16 + 8 * len(budgets)
-    path_ms = kern_ms                     # per-call device time (events around each launch)
+    path_ms = kern_ms                     # per-call device time (events around each launch, or the
+                                          # per-step time when consecutive calls overlap)
     achieved = alg_bytes / (path_ms / 1000.0) / 1e9
     # one extra traced step (untimed): the fused path records its single launch; the
     # two-kernel pipeline records per chunk K1 (internal stream) and K2+K3 (caller stream)
@@ -407,8 +426,9 @@ def main():
     traffic = load_traffic(a.config, batch)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
             "frac": achieved / peak_gbs, "traffic": traffic,
-            "kernel": "cm2::fused_kernel: the whole a1-a7 path in one launch per step (CUDA events around "
-                      "each call on the launching stream)",
+            "kernel": "cm2::fused_kernel: the whole a1-a7 path in one launch per step (" +
+                      ("CUDA events around each call on the launching stream" if events else
+                       "consecutive launches overlap (CM_EVAL_OVERLAP): timed region / steps") + ")",
             "alg_bytes_per_launch": alg_bytes, "ms_per_launch": path_ms, "kernels": kernels,
             "peak_source": peak_src}
     if a.samples:
@@ -439,7 +459,9 @@ def main():
                                       else f"theta={thetas}") + f", {len(budgets)} budgets",
                        "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
                        "parallelism": f"candidates sharded over {world} GPU(s), NCCL MIN all-reduce of keys",
-                       "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush"},
+                       "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush",
+                       "calls": ("overlapped: CM_EVAL_OVERLAP | CM_EVAL_INIT_KEYS, two alternating output "
+                                 "sets" if overlap else "serial: keys filled by the caller before each call")},
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks,
             "best": [cm.decode_key(k, cm.key_idx_bits(total)) for k in best]}

@@ -113,7 +113,19 @@ typedef struct {
                                atomicMin of ((2^31-1 - B_max) << idx_bits) | idx into caller-
                                initialised CM_KEY_NONE; needs idx_bits <= 32 (else CM_ERANGE) */
   int64_t cost_limit;       /* Eq. 13's bound 2 sum_fwd C + sum_bwd C, supplied by the caller */
+  int32_t flags;            /* 0 or an OR of:
+                               CM_EVAL_INIT_KEYS  the call itself sets best_key (and best_batch_key)
+                                 to CM_KEY_NONE before reducing into them (no caller fill needed);
+                               CM_EVAL_OVERLAP    the call may start while the kernel enqueued just
+                                 before it on `stream` is still finishing (programmatic dependent
+                                 launch: a batch's first S* stream in while the previous call's last
+                                 scan tasks drain).  The caller asserts that the work enqueued before
+                                 the call writes none of its inputs and touches none of its outputs
+                                 (peak, cost, keys, masks) -- e.g. the previous call of a loop that
+                                 alternates two output sets.  Ignored with a caller `workspace`. */
 } cm_eval_args;
+#define CM_EVAL_INIT_KEYS 1
+#define CM_EVAL_OVERLAP 2
 
 /*
  * cm_round_and_evaluate -- a1..a7 for every (S*, theta) candidate of one batch.

@@ -190,7 +190,7 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
                        index_base: int = 0, total_candidates: int | None = None,
                        best_key=None, masks: bool = False, peak=None, cost=None, stream=None,
                        samples: int | None = None, seed: int = 0, cost_limit: int | None = None,
-                       best_batch_key=None):
+                       best_batch_key=None, init_keys: bool = False, overlap: bool = False):
     """cm_round_and_evaluate on device tensors.
 
     sstar : float32 CUDA tensor; dense [N_S, n, ld] or tri4 [N_S, tri4_size(n)] (or any
@@ -201,6 +201,10 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     budget: int64 CUDA tensor [N_B] or None.
     cost_limit: with budgets, also run the max-batch epilogue (Eq. 13; the key of the largest
             B_max per budget among candidates with cost <= cost_limit, in ``best_batch_key``).
+    init_keys: the call sets best_key / best_batch_key to CM_KEY_NONE itself (CM_EVAL_INIT_KEYS).
+    overlap: the call may start while the previous kernel on the stream drains
+            (CM_EVAL_OVERLAP): only when that work writes none of this call's inputs and touches
+            none of its outputs, e.g. consecutive calls alternating two output sets.
     Returns dict(peak, cost, best_key, idx_bits, r_mask, s_mask) of CUDA tensors.
     Asynchronous on ``stream`` (default: torch's current stream).
     """
@@ -252,6 +256,7 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     a.seed = int(seed) & ((1 << 64) - 1)
     a.best_batch_key = _ptr(best_batch_key)
     a.cost_limit = int(cost_limit) if cost_limit is not None else 0
+    a.flags = (_abi.CM_EVAL_INIT_KEYS if init_keys else 0) | (_abi.CM_EVAL_OVERLAP if overlap else 0)
     a.n_budget = n_budget
     a.budget = _ptr(budget)
     a.index_base = int(index_base)

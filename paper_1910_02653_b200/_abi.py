@@ -20,6 +20,8 @@ CM_LAYOUT_TRI4 = 1
 CM_KEY_NONE = (1 << 63) - 1
 CM_ROUND_THRESHOLD = 0
 CM_ROUND_RANDOMIZED = 1
+CM_EVAL_INIT_KEYS = 1
+CM_EVAL_OVERLAP = 2
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
            "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
@@ -51,6 +53,7 @@ class EvalArgs(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("best_batch_key", ctypes.c_void_p),
         ("cost_limit", ctypes.c_int64),
+        ("flags", ctypes.c_int32),
     ]
 
 

@@ -95,6 +95,11 @@ struct cm_graph {
   cudaStream_t st_round = nullptr;
   cudaEvent_t ev_start = nullptr, ev_round[2] = {nullptr, nullptr}, ev_scan[2] = {nullptr, nullptr};
   bool used[2] = {false, false};
+  // fused path: the graph's workspace is used as two halves, alternating per call, each
+  // [control words][ring]; a half's control words are zero after every fused call on it
+  // (the kernel clears them on exit), so a CM_EVAL_OVERLAP call skips the memset
+  int ws_half = 0;
+  bool ctl_clean[2] = {false, false};
   std::mutex mu;
 };
 
@@ -103,7 +108,7 @@ int kernel_choice() {                 // CM_KERNEL=v1 selects the row-form kerne
   const char* e = std::getenv("CM_KERNEL");
   return (e && std::strcmp(e, "v1") == 0) ? 1 : 2;
 }
-constexpr int64_t kDefaultWsBytes = int64_t(512) << 20;  // two 256 MB chunk buffers: ~6 waves of scan tasks per chunk
+constexpr int64_t kDefaultWsBytes = int64_t(1024) << 20; // two 512 MB chunk buffers / fused ring halves
 }  // namespace
 
 
@@ -218,6 +223,20 @@ const void* fused_fn(int nt, bool bulk, bool rnd, bool s32) {
     default: return CM_F(4, int64_t);
   }
 #undef CM_F
+}
+
+__global__ void init_keys_kernel(int64_t* best_key, int64_t* best_batch_key, int n_budget) {
+  for (int b = threadIdx.x; b < n_budget; b += blockDim.x) {
+    best_key[b] = INT64_MAX;
+    if (best_batch_key) best_batch_key[b] = INT64_MAX;
+  }
+}
+// CM_EVAL_INIT_KEYS on the launch paths that do not initialise the keys in-kernel
+cudaError_t init_keys(const cm_eval_args* a, cudaStream_t st) {
+  if (!(a->flags & CM_EVAL_INIT_KEYS) || a->n_budget <= 0) return cudaSuccess;
+  init_keys_kernel<<<1, 256, 0, st>>>(a->best_key, a->best_batch_key, a->n_budget);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t idx_bits) {
@@ -411,15 +430,20 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     // slot predecessors must lie two windows back (W <= R / 2) or a warp blocked on one
     // window task can hold the ticket that would free its slot: clamped below.
     int64_t win = std::max<int64_t>(0, std::min<int64_t>(env_flag("CM_WIN", 0), 256));
-    int64_t ring_max = env_flag("CM_RING", 768);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
+    int64_t ring_max = std::min<int64_t>(env_flag("CM_RING", 768), 4096);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
     int64_t R = std::min<int64_t>(ring_max, units);
-    auto ctl_bytes = [](int64_t r) { return (4 * (2 + 3 * r) + 255) & ~int64_t(255); };
-    while (R > 1 && ctl_bytes(R) + R * slot_bytes > ws_bytes) --R;
+    auto ctl_bytes = [](int64_t r) { return (4 * cm2::fused_ctl_words(r) + 255) & ~int64_t(255); };
+    // the graph's own workspace: two halves used alternately (CM_EVAL_OVERLAP needs the
+    // previous call's ring intact); a caller workspace: one
+    const bool own_ws = a->workspace == nullptr;
+    const int64_t set_bytes = own_ws ? (ws_bytes / 2) & ~int64_t(255) : ws_bytes;
+    const bool overlap = own_ws && (a->flags & CM_EVAL_OVERLAP);
+    while (R > 1 && ctl_bytes(R) + R * slot_bytes > set_bytes) --R;
     if (R < units) win = std::min<int64_t>(win, R / 2);             // no slot reuse: any order is safe
     const int64_t total_tasks = win > 0 ? ((units + win - 1) / win) * win * (int64_t)G * nt
                                         : (units - 1) * (int64_t)G * nt +
                                               (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
-    if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= ws_bytes &&
+    if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= set_bytes &&
         total_tasks < (int64_t(1) << 31)) {
       const void* fn = fused_fn(nt, bulk, rnd, g->scan32);
       {
@@ -444,9 +468,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         fp.sp = sp;
         fp.sp.warp_bytes = (int32_t)wbf;
         fp.qp = qp;
-        uint32_t* ctl = reinterpret_cast<uint32_t*>(ws);
-        fp.ctl = ctl;
-        fp.ring = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + ctl_bytes(R));
+        fp.init_keys = (a->flags & CM_EVAL_INIT_KEYS) && a->n_budget > 0;
         fp.slot_words = slot_bytes / 4;
         fp.n_slots = (int32_t)R;
         fp.n_sstar = a->n_sstar;
@@ -475,14 +497,35 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           if (fp.task_claim < 1 || fp.tpu % fp.task_claim || win > 0) fp.task_claim = 1;
         }
         std::lock_guard<std::mutex> lock(g->mu);
-        e = cudaMemsetAsync(ctl, 0, 4 * (size_t)(2 + 3 * R), st);
-        if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
+        const int half = own_ws ? g->ws_half : 0;
+        unsigned char* set_base = reinterpret_cast<unsigned char*>(ws) + half * set_bytes;
+        uint32_t* ctl = reinterpret_cast<uint32_t*>(set_base);
+        fp.ctl = ctl;
+        fp.ring = reinterpret_cast<uint32_t*>(set_base + ctl_bytes(R));
+        if (!overlap || !g->ctl_clean[half] || fp.trace) {
+          e = cudaMemsetAsync(ctl, 0, 4 * (size_t)cm2::fused_ctl_words(R), st);
+          if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
+        }
         void* args[] = {&fp, &tmap, &dmaps};
         const bool tr = trace_enabled();
         g_trace.used = 0;
         if (tr) cudaEventRecord(trace_event(0), st);
-        e = cudaLaunchKernel(fn, dim3((unsigned)g->sm_count), dim3((unsigned)threads), args, smemf, st);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)g->sm_count);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = smemf;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = overlap ? 1 : 0;
+        e = cudaLaunchKernelExC(&cfg, fn, args);
         if (e != cudaSuccess) return cuda_fail(e, "launch fused_kernel");
+        if (own_ws) {
+          g->ctl_clean[half] = true;                 // cleared by the kernel's last CTA
+          g->ws_half ^= 1;
+        }
         if (tr) {                                    // one "chunk": K1 and K2 share the launch
           cudaEventRecord(trace_event(1), st);
           cudaEventRecord(trace_event(2), st);
@@ -498,9 +541,12 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   const int64_t half = cap * cand_bytes(n, m32);
   std::lock_guard<std::mutex> lock(g->mu);
+  if (!a->workspace) g->ctl_clean[0] = g->ctl_clean[1] = false;     // chunk buffers overwrite them
   const bool tr = trace_enabled();
   g_trace.used = 0;
   g_launches = 0;
+  e = init_keys(a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "init keys");
   e = cudaEventRecord(g->ev_start, st);                       // inputs written on `st` before the call
   if (e == cudaSuccess) e = cudaStreamWaitEvent(g->st_round, g->ev_start, 0);
   int c = 0;
@@ -941,7 +987,10 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
   g_launches = 0;
-  if (n_cand == 0) return CM_OK;
+  if (n_cand == 0) {
+    const cudaError_t e0 = init_keys(a, reinterpret_cast<cudaStream_t>(stream));
+    return e0 == cudaSuccess ? CM_OK : cuda_fail(e0, "init keys");
+  }
   if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(g->n_slot, g->scan32, false) <= (size_t)g->smem_optin) {
     cudaError_t e0 = cudaGetLastError();                 // surface earlier asynchronous faults
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
@@ -1015,8 +1064,10 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   p.r_mask = a->r_mask;
   p.s_mask = a->s_mask;
   p.tri_words = tri_words;
+  e = init_keys(a, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "init keys");
   cmk::round_evaluate_kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(p);
-  g_launches = 1;
+  ++g_launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "launch round_evaluate_kernel");
   return CM_OK;

@@ -1205,7 +1205,9 @@ struct FusedParams {
   int64_t slot_words;         // 32 n_theta cs words of candidate blocks, then the partials
   int32_t n_slots;
   uint32_t* ctl;              // [0] task ticket, [1 + slot] filled, [1 + R + slot] done,
-                              // [1 + 2R + slot] freed, [1 + 3R] S* ticket (zeroed per call)
+                              // [1 + 2R + slot] freed, [1 + 3R] S* ticket, [2 + 3R] CTAs
+                              // exited, [3 + 3R] key-init state; fused_ctl_words(R) words, zero
+                              // at launch and zeroed again by the last CTA to exit
   int32_t n_sstar, n_theta;
   int32_t n_units;
   int32_t tpu;                // tasks of a full unit: G * n_theta
@@ -1214,7 +1216,28 @@ struct FusedParams {
   int32_t task_claim;         // scan tasks per consumer ticket (divides tpu)
   int32_t win_units;          // ticket windows (units), 0: unit-major order
   uint64_t* trace;            // debug (CM_TRACE=2): per CTA {start, K1 end, ~first unit-0 task, K2 end} ns
+  int32_t init_keys;          // CM_EVAL_INIT_KEYS: the first CTA sets the keys to INT64_MAX
 };
+__host__ __device__ constexpr int64_t fused_ctl_words(int64_t R) { return 4 + 3 * R; }
+
+// Kernel exit: every warp of the CTA (both roles) has stopped touching the control words;
+// the last CTA out zeroes them, so the next call on this workspace half can skip the memset
+// (and start while this one drains: CM_EVAL_OVERLAP).
+__device__ __forceinline__ void fused_exit(const FusedParams& fp) {
+  __shared__ uint32_t last;
+  asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
+  const int64_t words = fused_ctl_words(fp.n_slots);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(fp.ctl + 2 + 3 * (int64_t)fp.n_slots, 1u) == gridDim.x - 1;
+  }
+  asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
+  if (last) {
+    __threadfence();
+    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) fp.ctl[i] = 0u;
+    __threadfence();
+  }
+}
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -1290,6 +1313,14 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const __grid_constant__ DiagMaps dmaps) {
   constexpr int KF1 = k1_warps(NT);
+  // warp roles: the rounding warps take the low (default) or, with CM_K1_HIGH, the high warp
+  // indices -- the SMSP arbiter favours higher warp ids
+#ifdef CM_K1_HIGH
+  constexpr bool kK1High = true;
+#else
+  constexpr bool kK1High = false;
+#endif
+  constexpr int kFirstScanWarp = kK1High ? 0 : KF1;
   extern __shared__ __align__(1024) unsigned char fraw[];
   unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
   unsigned char* k1smem = base;
@@ -1297,10 +1328,21 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& sp = fp.sp;
+  // a dependent launch (the next call, CM_EVAL_OVERLAP) may take SMs as soon as they free up
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (fp.init_keys && threadIdx.x == 0 &&
+      atomicCAS(fp.ctl + 3 + 3 * (int64_t)fp.n_slots, 0u, 1u) == 0u) {       // first CTA in
+    for (int b = 0; b < fp.qp.n_budget; ++b) {
+      fp.qp.best_key[b] = INT64_MAX;
+      if (fp.qp.best_batch_key) fp.qp.best_batch_key[b] = INT64_MAX;
+    }
+    __threadfence();
+    atomicExch(fp.ctl + 3 + 3 * (int64_t)fp.n_slots, 2u);
+  }
   k1_setup<NT, BULK, RAND>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
   for (int i = threadIdx.x; i < sp.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(k2smem)[i] = sp.blob[i];
-  if (warp == KF1) {
+  if (warp == kFirstScanWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
                  :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_base)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -1310,15 +1352,17 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (fp.trace && threadIdx.x == 0) fp.trace[4 * blockIdx.x] = globaltimer();
 
-  if (warp < KF1) {                                                 // ---- rounding (K1) warps
+  if (kK1High ? warp >= kFusedScanWarps : warp < KF1) {             // ---- rounding (K1) warps
     __shared__ int sq[KF1][8];
+    const int w1 = kK1High ? warp - kFusedScanWarps : warp;
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
-    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, warp, sq[warp], hk);
+    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, w1, sq[w1], hk);
     if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 1), globaltimer());
+    fused_exit(fp);
     return;
   }
   // ---- scan (K2) warps
-  const int wk = warp - KF1;
+  const int wk = warp - kFirstScanWarp;
   const ScanCtx<ET, true> x = scan_ctx<ET, true>(sp, k2smem, wk, tmem_base, kFusedTmemCols);
   const int G = sp.G;
   const int R = fp.n_slots;
@@ -1367,6 +1411,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   // A ticket covers tc consecutive tasks (tc divides tpu, so a claim stays inside one unit):
   // small graphs take a whole unit per ticket and pay the fence and the count once per unit.
   const uint32_t tc = (uint32_t)fp.task_claim;
+  bool keys_ready = false;
   uint32_t t = claim();
   while ((int64_t)t * tc < fp.total_tasks) {
     const uint32_t t_next = claim();
@@ -1411,6 +1456,10 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     if (lane == 0) old = atomicAdd(fp.ctl + 1 + R + slot, cnt);
     old = __shfl_sync(FULL, old, 0);
     if (old + cnt == (uint32_t)fp.tpu * (uint32_t)k + tasks_u) {     // last task of unit u: reduce it
+      if (fp.init_keys && !keys_ready) {                            // the keys are initialised
+        warp_wait_geq(fp.ctl + 3 + 3 * R, 2u);
+        keys_ready = true;
+      }
       __threadfence();
       for (int64_t c = lane; c < ncand; c += 32) reduce_one(fp.qp, part, c, (int64_t)u * unit_cands);
       __threadfence();                                              // partials read: release the slot
@@ -1424,8 +1473,9 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 3), globaltimer());
   asm volatile("bar.sync 1, %0;" :: "r"(32 * kFusedScanWarps) : "memory");   // the scan warps only
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == KF1)
+  if (warp == kFirstScanWarp)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem_base) : "memory");
+  fused_exit(fp);
 }
 
 }  // namespace cm2
