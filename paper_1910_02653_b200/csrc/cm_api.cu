@@ -99,7 +99,7 @@ struct cm_graph {
   // [control words][ring]; a half's control words are zero after every fused call on it
   // (the kernel clears them on exit), so a CM_EVAL_OVERLAP call skips the memset
   int ws_half = 0;
-  bool ctl_clean[2] = {false, false};
+  int64_t ctl_clean[2] = {0, 0};      // leading control words of each half known to be zero
   std::mutex mu;
 };
 
@@ -502,7 +502,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         uint32_t* ctl = reinterpret_cast<uint32_t*>(set_base);
         fp.ctl = ctl;
         fp.ring = reinterpret_cast<uint32_t*>(set_base + ctl_bytes(R));
-        if (!overlap || !g->ctl_clean[half] || fp.trace) {
+        // (a call with a smaller ring left ring data where this call's control words lie)
+        if (!overlap || g->ctl_clean[half] < cm2::fused_ctl_words(R) || fp.trace) {
           e = cudaMemsetAsync(ctl, 0, 4 * (size_t)cm2::fused_ctl_words(R), st);
           if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
         }
@@ -523,7 +524,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         e = cudaLaunchKernelExC(&cfg, fn, args);
         if (e != cudaSuccess) return cuda_fail(e, "launch fused_kernel");
         if (own_ws) {
-          g->ctl_clean[half] = true;                 // cleared by the kernel's last CTA
+          g->ctl_clean[half] = cm2::fused_ctl_words(R);   // cleared by the kernel's last CTA
           g->ws_half ^= 1;
         }
         if (tr) {                                    // one "chunk": K1 and K2 share the launch
@@ -541,7 +542,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   const int64_t half = cap * cand_bytes(n, m32);
   std::lock_guard<std::mutex> lock(g->mu);
-  if (!a->workspace) g->ctl_clean[0] = g->ctl_clean[1] = false;     // chunk buffers overwrite them
+  if (!a->workspace) g->ctl_clean[0] = g->ctl_clean[1] = 0;         // chunk buffers overwrite them
   const bool tr = trace_enabled();
   g_trace.used = 0;
   g_launches = 0;

@@ -44,9 +44,10 @@ def check_keys(key, peak, cost, budgets, bits, index_base):
 
 
 def run_chain(g, layout, n_calls, N, before=None):
-    """n_calls overlapped calls, call i on its own S* batch (generator seed 100 + i) and its
-    own outputs, keys pre-filled with 0 (a value INIT_KEYS must overwrite).  `before(i)` may
-    enqueue other work between calls."""
+    """n_calls overlapped calls, call i on its own S* batch (generator seed 100 + i, N[i] S*,
+    or N for all) and its own outputs, keys pre-filled with 0 (a value INIT_KEYS must
+    overwrite).  `before(i)` may enqueue other work between calls."""
+    Ns = list(N) if isinstance(N, (list, tuple)) else [N] * n_calls
     import torch
     import paper_1910_02653_b200 as cm
     from workloads.device_gen import DeviceGenerator
@@ -58,7 +59,7 @@ def run_chain(g, layout, n_calls, N, before=None):
     ins, outs = [], []
     for i in range(n_calls):
         dg = DeviceGenerator(g, "g1", 100 + i, layout=layout)
-        x = torch.empty(dg.shape(N), dtype=torch.float32, device=dev)
+        x = torch.empty(dg.shape(Ns[i]), dtype=torch.float32, device=dev)
         dg.fill(x, 0)
         ins.append(x)
     torch.cuda.synchronize()
@@ -67,18 +68,19 @@ def run_chain(g, layout, n_calls, N, before=None):
             before(i)
         key = torch.zeros(len(budgets), dtype=torch.int64, device=dev)
         outs.append(cm.round_and_evaluate(graph, ins[i], th, bu, layout=layout, best_key=key,
-                                          index_base=1000 * i, total_candidates=1000 * n_calls,
+                                          index_base=2000 * i, total_candidates=2000 * n_calls,
                                           init_keys=True, overlap=True))
     torch.cuda.synchronize()
     inst = Instance.from_graph(g)
     for i, out in enumerate(outs):
+        N = Ns[i]
         peak, cost = out["peak"].cpu().numpy(), out["cost"].cpu().numpy()
-        for s in sorted({0, 31, 32, N // 2, N - 1}):
+        for s in sorted(v for v in {0, 31, 32, N // 2, N - 1} if v < N):
             x = gen_sstar(g, "g1", 100 + i, s, 1)[0]
             for j, t in enumerate([0.5, 0.3]):
                 o = evaluate(inst, x, t)
                 assert (peak[2 * s + j], cost[2 * s + j]) == (o["peak"], o["cost"]), (i, s, j)
-        check_keys(out["best_key"].cpu().numpy(), peak, cost, budgets, out["idx_bits"], 1000 * i)
+        check_keys(out["best_key"].cpu().numpy(), peak, cost, budgets, out["idx_bits"], 2000 * i)
     graph.close()
     return outs
 
@@ -111,6 +113,13 @@ def test_overlap_after_other_paths(env_var):
     env_var(CM_FUSED=1)
     run_chain(G.vgg16(), "dense", 6, 300, before)
     assert cm.debug_last_launches() == 1
+
+
+@pytest.mark.timeout(240)
+def test_overlap_ring_sizes_change():
+    """Batches of 2 to 1000 S* (rings of 1 to 32 slots): a half's previous call had a smaller
+    ring, so its ring data lies where the next call's control words go (they must be cleared)."""
+    run_chain(G.resnet50(), "dense", 8, [40, 60, 1000, 700, 2, 33, 900, 64])
 
 
 @pytest.mark.parametrize("kernel", ["fused", "pipeline", "v1"])
