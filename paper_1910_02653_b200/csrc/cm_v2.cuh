@@ -1462,6 +1462,12 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
       }
       __threadfence();
       for (int64_t c = lane; c < ncand; c += 32) reduce_one(fp.qp, part, c, (int64_t)u * unit_cands);
+#ifdef CM_DISCARD
+      // the slot's data is dead: drop its L2 lines without writing them back to DRAM
+      __syncwarp();
+      for (int64_t l = lane; l < fp.slot_words / 32; l += 32)
+        asm volatile("discard.global.L2 [%0], 128;" :: "l"(ws + 32 * l) : "memory");
+#endif
       __threadfence();                                              // partials read: release the slot
       __syncwarp();
       if (lane == 0) atomicAdd(fp.ctl + 1 + 2 * R + slot, 1u);
