@@ -385,6 +385,7 @@ def main():
                "h2d_bytes_per_step": eb * egen.stride * 4,
                "d2h_bytes_per_step": eb * n_theta * 16 + 8 * len(budgets),
                "batch_per_gpu": eb, "host_memory": "pinned", "layout": "tri4",
+               "h2d_gb_per_s": eb * egen.stride * 4 * e_steps / e_dt / 1e9,
                "note": "PCIe-bound: the S* bytes cross the host link every step"}
 
     if rank != 0:

@@ -100,3 +100,31 @@ def test_binding_imports_and_fails_loudly(tmp_path):
     from paper_1910_02653_b200 import _abi
     with pytest.raises(ImportError):
         _abi.load(str(tmp_path / "missing.so"))
+
+
+def test_eval_args_layout_matches_binding(tmp_path):
+    """The ctypes mirror of cm_eval_args has the header's fields, offsets and size (a C
+    program compiled against include/cm.h prints them), and the #define constants agree."""
+    import shutil
+    import subprocess
+    from paper_1910_02653_b200 import _abi
+    src = open(os.path.join(ROOT, "include", "cm.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} cm_eval_args;", src, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"([A-Za-z_][A-Za-z0-9_]*)\s*;", body)
+    assert fields == [f for f, _ in _abi.EvalArgs._fields_]
+    for name in ("CM_LAYOUT_DENSE", "CM_LAYOUT_TRI4", "CM_ROUND_THRESHOLD", "CM_ROUND_RANDOMIZED",
+                 "CM_EVAL_INIT_KEYS", "CM_EVAL_OVERLAP"):
+        m = re.search(r"#define\s+%s\s+(\d+)" % name, src)
+        assert m and int(m.group(1)) == getattr(_abi, name), name
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    prog = tmp_path / "layout.c"
+    prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "cm.h"\nint main(void) {\n'
+                    + "".join(f'  printf("%zu\\n", offsetof(cm_eval_args, {f}));\n' for f in fields)
+                    + '  printf("%zu\\n", sizeof(cm_eval_args));\n  return 0;\n}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [getattr(_abi.EvalArgs, f).offset for f in fields] + [ctypes.sizeof(_abi.EvalArgs)]
+    assert got == want

@@ -151,3 +151,42 @@ def test_init_keys_all_paths(env_var, kernel):
     torch.cuda.synchronize()
     assert (key.cpu().numpy() == KEY_NONE).all()
     graph.close()
+
+
+@pytest.mark.timeout(240)
+def test_overlap_randomized_and_max_batch():
+    """Overlapped calls with randomized rounding (2 samples per S*) and the max-batch epilogue,
+    keys and batch keys initialised in-kernel over pre-filled zeros, equal to serial calls with
+    caller-initialised keys (the serial path is checked against the oracle elsewhere)."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    g = G.resnet50()
+    budgets = B.geometric_grid(g, 6)
+    bu = torch.tensor(budgets, device="cuda")
+    limit = B.eq13_cost_limit(g)
+    graph = cm.Graph.from_workload(g)
+    ins = []
+    for i in range(4):
+        dg = DeviceGenerator(g, "g1", 300 + i, layout="dense")
+        x = torch.empty(dg.shape(250), dtype=torch.float32, device="cuda")
+        dg.fill(x, 0)
+        ins.append(x)
+
+    def call(i, overlap):
+        z = (lambda: torch.zeros(len(budgets), dtype=torch.int64, device="cuda")) if overlap else \
+            (lambda: torch.full((len(budgets),), KEY_NONE, dtype=torch.int64, device="cuda"))
+        return cm.round_and_evaluate(graph, ins[i], None, bu, samples=2, seed=99, index_base=500 * i,
+                                     total_candidates=2000, best_key=z(), best_batch_key=z(),
+                                     cost_limit=limit, init_keys=overlap, overlap=overlap)
+    over = [call(i, True) for i in range(4)]
+    torch.cuda.synchronize()
+    serial = []
+    for i in range(4):
+        serial.append(call(i, False))
+        torch.cuda.synchronize()
+    for a, b in zip(over, serial):
+        for k in ("peak", "cost", "best_key", "best_batch_key"):
+            assert torch.equal(a[k], b[k]), k
+    assert any(int(k) != KEY_NONE for k in over[0]["best_batch_key"].cpu())
+    graph.close()
