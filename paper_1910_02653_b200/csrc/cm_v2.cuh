@@ -1225,6 +1225,12 @@ __host__ __device__ constexpr int64_t fused_ctl_words(int64_t R) { return 4 + 3 
 // (and start while this one drains: CM_EVAL_OVERLAP).
 __device__ __forceinline__ void fused_exit(const FusedParams& fp) {
   __shared__ uint32_t last;
+  // Let the next call (CM_EVAL_OVERLAP) be scheduled -- its CTAs then take SMs as this call's
+  // CTAs exit -- but only once the call before this one has completed: the next call reuses
+  // that call's workspace half, and a CTA that cannot get TMEM yet may already be resident
+  // when shared memory allows two CTAs per SM, so residency alone does not order them.
+  // Thread 0 (rounding warp 0) gets here when its production ends, well before the tail.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
   const int64_t words = fused_ctl_words(fp.n_slots);
   if (threadIdx.x == 0) {
@@ -1328,8 +1334,6 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& sp = fp.sp;
-  // a dependent launch (the next call, CM_EVAL_OVERLAP) may take SMs as soon as they free up
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (fp.init_keys && threadIdx.x == 0 &&
       atomicCAS(fp.ctl + 3 + 3 * (int64_t)fp.n_slots, 0u, 1u) == 0u) {       // first CTA in
     for (int b = 0; b < fp.qp.n_budget; ++b) {
