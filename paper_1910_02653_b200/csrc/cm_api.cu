@@ -484,11 +484,14 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           if (g_cta_trace) cudaMemsetAsync(g_cta_trace, 0, 4 * sizeof(uint64_t) * g->sm_count, st);
           fp.trace = g_cta_trace;
         }
-        {  // ~64 blocks of rounding work per ticket: 8 S* at n = 89, 1 at n = 353
+        {  // S* per producer ticket: 8 at n = 89, 2 at n = 213 .. ~420, 1 above
           const int gr = n >= 2 ? (n - 2) / 32 + 1 : 1;
           const int blocks = gr * (gr + 1) / 2;
           int c = 1;
           while (c < 8 && 2 * c * blocks <= 64) c *= 2;
+          // measured with overlapped calls: n = 353 (66 blocks) 19.55 vs 19.0-19.35 M cand/s at
+          // 2 S* per ticket, n = 401 (91) 14.72 vs 14.66; n = 563 (171) better at 1
+          if (c == 1 && 2 * blocks <= 190) c = 2;
           fp.claim = env_flag("CM_CLAIM", c);
           if (fp.claim < 1 || fp.claim > 32 || (fp.claim & (fp.claim - 1))) fp.claim = c;
           // scan tasks per consumer ticket (tuning; 1: measured a whole VGG16 unit per ticket
