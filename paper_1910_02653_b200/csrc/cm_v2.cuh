@@ -508,8 +508,17 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
             // t is clamped to [0, 2^24] (x > 1 or inf: always; x <= 0: never) and NaN converts to 0
             const float xs = x[q] * 16777216.0f;
             const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
+            if (NT >= 2) {
+              // (w >> 8) < t  <=>  w <= 256 t - 1 for t >= 1 (t = 2^24 wraps to 2^32 - 1:
+              // always); t = 0: never.  One compare per sample instead of shift + compare
+              // (measured 4 samples 8.70 vs 8.57 M cand/s; 1 sample: slower, kept below)
+              const uint32_t tw = (t << 8) - 1u;
+              const uint32_t qb = t != 0u ? (1u << q) : 0u;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) rw[j] |= (ow[j] >> 8) < t ? (1u << q) : 0u;
+              for (int j = 0; j < NT; ++j) rw[j] |= ow[j] <= tw ? qb : 0u;
+            } else {
+              rw[0] |= (ow[0] >> 8) < t ? (1u << q) : 0u;
+            }
           }
 #pragma unroll
           for (int j = 0; j < NT; ++j) word[j] = rw[j] & rmask;
