@@ -453,10 +453,11 @@ def test_int32_state_near_limit(layout):
 
 
 def test_bench_launch_configuration_sampled():
-    """The exact launch bench.py times: ResNet-50 (n=353), 125 000 device-generated G1 S* in the
-    dense layout with 128-byte rows (ld = 384), theta 0.5, 16 budgets, one fused launch;
-    sampled candidates against the oracle, every per-budget key against the GPU's own
-    per-candidate outputs."""
+    """The exact launches bench.py times: ResNet-50 (n=353), 125 000 device-generated G1 S* in
+    the dense layout with 128-byte rows (ld = 384), theta 0.5, 16 budgets, one fused launch per
+    step, consecutive steps overlapped (CM_EVAL_OVERLAP | CM_EVAL_INIT_KEYS) on two alternating
+    output sets whose keys start at 0; three steps, the last two checked: sampled candidates
+    against the oracle, every per-budget key against the GPU's own per-candidate outputs."""
     import torch
     import paper_1910_02653_b200 as cm
     from workloads.device_gen import DeviceGenerator
@@ -467,24 +468,34 @@ def test_bench_launch_configuration_sampled():
     dg.fill(buf, 0)
     graph = cm.Graph.from_workload(g)
     budgets = B.geometric_grid(g, 16)
-    out = cm.round_and_evaluate(graph, buf, torch.tensor([0.5], device="cuda"), torch.tensor(budgets, device="cuda"))
+    th = torch.tensor([0.5], device="cuda")
+    bu = torch.tensor(budgets, device="cuda")
+    sets = [{k: torch.zeros(n, dtype=torch.int64, device="cuda") for k, n in
+             (("peak", N), ("cost", N), ("key", len(budgets)))} for _ in range(2)]
+    for step in range(3):
+        o = sets[step % 2]
+        o["key"].zero_()
+        out = cm.round_and_evaluate(graph, buf, th, bu, best_key=o["key"], peak=o["peak"], cost=o["cost"],
+                                    init_keys=True, overlap=True)
+        assert cm.debug_last_launches() == 1
     torch.cuda.synchronize()
-    assert cm.debug_last_launches() == 1
-    peak, cost = out["peak"].cpu().numpy(), out["cost"].cpu().numpy()
     del buf
     inst = Instance.from_graph(g)
     rng = np.random.default_rng(7)
-    for s in sorted(set(rng.integers(0, N, 14).tolist()) | {0, 31, 32, N - 1}):
-        o = evaluate(inst, gen_sstar(g, "g1", 20250101, s, 1)[0], 0.5)
-        assert (peak[s], cost[s]) == (o["peak"], o["cost"]), s
+    samples = sorted(set(rng.integers(0, N, 14).tolist()) | {0, 31, 32, N - 1})
+    want = {s: evaluate(inst, gen_sstar(g, "g1", 20250101, s, 1)[0], 0.5) for s in samples}
     bits = out["idx_bits"]
-    for b, key in enumerate(out["best_key"].cpu().numpy()):
-        feas = np.nonzero(peak <= budgets[b])[0]
-        if len(feas) == 0:
-            assert key == KEY_NONE
-            continue
-        c = cost[feas].min()
-        assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, feas[cost[feas] == c].min())
+    for o in sets:
+        peak, cost = o["peak"].cpu().numpy(), o["cost"].cpu().numpy()
+        for s in samples:
+            assert (peak[s], cost[s]) == (want[s]["peak"], want[s]["cost"]), s
+        for b, key in enumerate(o["key"].cpu().numpy()):
+            feas = np.nonzero(peak <= budgets[b])[0]
+            if len(feas) == 0:
+                assert key == KEY_NONE
+                continue
+            c = cost[feas].min()
+            assert (int(key) >> bits, int(key) & ((1 << bits) - 1)) == (c, feas[cost[feas] == c].min())
 
 
 @pytest.mark.timeout(240)
