@@ -131,9 +131,30 @@ typedef struct {
  * cm_round_and_evaluate -- a1..a7 for every (S*, theta) candidate of one batch.
  * Stream-ordered and asynchronous on `stream`: no host synchronisation, no
  * allocation.  CM_ERANGE if total_candidates needs so many index bits that the
- * cost bound no longer fits the key (cost_bound >= 2^(63 - idx_bits)).
+ * cost bound no longer fits the key (cost_bound >= 2^(63 - idx_bits)).  The graph's
+ * device (current at cm_graph_create) must be the current device (else CM_EINVAL).
+ * Every call is numbered (cm_last_call_seq) and signals its completion on the device
+ * (cm_stream_wait_call).
  */
 cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* args, cm_stream stream);
+
+/*
+ * Completion signal without a stream event (a8 plumbing).  Every
+ * cm_round_and_evaluate call on g gets the next sequence number (1, 2, ...; 32-bit,
+ * wrapping); when all of its outputs (peak, cost, keys, masks) are written, the device
+ * stores that number into a word the graph owns: the fused persistent kernel's last CTA
+ * does it (a release store at system scope), the multi-kernel paths with a stream write
+ * after their last launch.  cm_stream_wait_call makes `stream` wait until call `seq` (or
+ * a later one) completed -- a stream memory operation (cuStreamWaitValue32, GEQ in
+ * wrap-around order): no kernel and no event on the calling stream, so a reduction of
+ * call i's keys on another stream does not stop call i+1 from overlapping call i
+ * (CM_EVAL_OVERLAP).  Calls on one graph must complete in call order (they do when
+ * they are issued to one stream).
+ *   cm_last_call_seq     the number of this graph's last cm_round_and_evaluate call (0: none)
+ *   cm_stream_wait_call  CM_EINVAL for NULL g; CM_ECUDA if the stream operation fails
+ */
+uint32_t cm_last_call_seq(const cm_graph* g);
+cm_status cm_stream_wait_call(const cm_graph* g, uint32_t seq, cm_stream stream);
 
 /* Bytes of workspace needed to process `chunk_candidates` candidates per internal chunk
  * (the library splits a batch into chunks that fit the workspace it is given). */
@@ -157,9 +178,13 @@ int32_t cm_debug_trace(float* out, int32_t max_values);
  * (1 on the fused persistent path; per chunk ceil(n_theta/4) + 2 on the two-kernel pipeline). */
 int32_t cm_debug_last_launches(void);
 /* Debug aid: with CM_TRACE=2, the fused kernel records per CTA {start, rounding warps done,
- * ~(first wait for unit 0 satisfied), scan warps done} in %globaltimer ns; after the call
- * completed this copies up to max_values of them and returns the count (0 if none). */
+ * ~(first wait for unit 0 satisfied), scan warps done} in %globaltimer ns, into one of 16
+ * per-call regions used in turn (the regions are cleared when the first is reused, so up to 16
+ * consecutive calls keep overlapping); after the call completed cm_debug_cta_trace copies up
+ * to max_values of the calling thread's last call's values and returns the count (0 if none);
+ * cm_debug_cta_trace_at does the same for the call `back` calls earlier (back < 16). */
 int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values);
+int32_t cm_debug_cta_trace_at(int32_t back, uint64_t* out, int32_t max_values);
 
 /*
  * Execution plans for chosen schedules.  Algorithm 1 "Generate execution
@@ -175,6 +200,10 @@ int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values);
  *   peak_out         receives the plan's peak (stage-boundary semantics: entering stage t exactly
  *                    the checkpoints S_t are resident; peak after each compute): the Eq. 6-9 peak
  *                    when hoist = 0, never higher when hoist = 1; may be NULL
+ * With hoist = 0 the plan is Alg. 1's literally: a value resident in stage t that no FREE_{t,i,k}
+ * deallocates (a checkpoint neither used in stage t nor kept for t+1) gets no
+ * statement; an interpreter must drop every value not in S_{t+1} at the end of stage t, the
+ * stage-boundary semantics the peak is computed under.  hoist = 1 emits those deallocations.
  * CM_EINVAL when the masks violate constraints (2) / (3); CM_ERANGE when capacity < *n_out. */
 typedef struct {
   int32_t op;     /* CM_OP_COMPUTE or CM_OP_DEALLOC */

@@ -177,6 +177,27 @@ def debug_trace(max_values: int = 4096):
 
 
 
+def debug_cta_trace(back: int = 0, max_values: int = 4 * 1024):
+    """CM_TRACE=2 per-CTA %globaltimer stamps of the calling thread's fused call `back` calls ago:
+    uint64 [CTAs][4] = {start, rounding warps done, ~(first unit-0 wait satisfied), scan warps done}."""
+    buf = (ctypes.c_uint64 * max_values)()
+    m = _lib.cm_debug_cta_trace_at(int(back), buf, max_values)
+    return np.frombuffer(buf, np.uint64, count=m).reshape(-1, 4).copy()
+
+
+def last_call_seq(graph: Graph) -> int:
+    """cm_last_call_seq: the number of the graph's last round_and_evaluate call."""
+    return int(_lib.cm_last_call_seq(graph.handle))
+
+
+def stream_wait_call(graph: Graph, seq: int, stream) -> None:
+    """cm_stream_wait_call: `stream` (a CUDA stream handle) waits until call `seq` on `graph`
+    has written all its outputs (a stream memory operation; nothing is enqueued on the stream
+    the call itself ran on)."""
+    _check(_lib.cm_stream_wait_call(graph.handle, int(seq) & 0xffffffff, ctypes.c_void_p(stream)),
+           "cm_stream_wait_call")
+
+
 def debug_last_launches() -> int:
     """Kernels launched by this thread's last round_and_evaluate call (cm_debug_last_launches)."""
     return int(_lib.cm_debug_last_launches())
@@ -229,6 +250,12 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     n_theta = int(samples) if randomized else theta.numel()
     n_cand = n_sstar * n_theta
     n_budget = 0 if budget is None else budget.numel()
+    if overlap and (peak is None or cost is None or (n_budget and best_key is None)
+                    or (cost_limit is not None and n_budget and best_batch_key is None)):
+        # an overlapped call may still be running the previous call's tail: outputs allocated
+        # here could reuse memory the caller just dropped that the previous call still writes
+        raise ValueError("overlap=True needs caller-owned peak, cost and best_key (and best_batch_key) "
+                         "that no call still in flight writes")
     if total_candidates is None:
         total_candidates = index_base + n_cand
     if peak is None:

@@ -24,7 +24,8 @@ CM_EVAL_INIT_KEYS = 1
 CM_EVAL_OVERLAP = 2
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
-           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
+           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_debug_cta_trace_at",
+           "cm_last_call_seq", "cm_stream_wait_call", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
            "cm_policy_checkpoints", "cm_policy_sstar", "cm_policy_last_error",
            "cm_last_error")
 
@@ -81,6 +82,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_debug_last_launches.restype = ctypes.c_int32
     lib.cm_debug_cta_trace.argtypes = [P, ctypes.c_int32]
     lib.cm_debug_cta_trace.restype = ctypes.c_int32
+    lib.cm_debug_cta_trace_at.argtypes = [ctypes.c_int32, P, ctypes.c_int32]
+    lib.cm_debug_cta_trace_at.restype = ctypes.c_int32
+    lib.cm_last_call_seq.argtypes = [P]
+    lib.cm_last_call_seq.restype = ctypes.c_uint32
+    lib.cm_stream_wait_call.argtypes = [P, ctypes.c_uint32, P]
+    lib.cm_stream_wait_call.restype = ctypes.c_int
     lib.cm_key_idx_bits.argtypes = [ctypes.c_int64]
     lib.cm_key_idx_bits.restype = ctypes.c_int32
     lib.cm_decode_key.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),

@@ -100,6 +100,9 @@ struct cm_graph {
   // (the kernel clears them on exit), so a CM_EVAL_OVERLAP call skips the memset
   int ws_half = 0;
   int64_t ctl_clean[2] = {0, 0};      // leading control words of each half known to be zero
+  // completion signal (cm_stream_wait_call): call i stores i into d_seq when its outputs are written
+  uint32_t* d_seq = nullptr;
+  uint32_t seq = 0;                   // number of the last call (under mu)
   std::mutex mu;
 };
 
@@ -118,6 +121,40 @@ namespace {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*StreamValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValue32Fn stream_value32(const char* name) {
+  void* ptr = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<StreamValue32Fn>(ptr);
+  return nullptr;
+}
+StreamValue32Fn wait_value32() {
+  static StreamValue32Fn fn = stream_value32("cuStreamWaitValue32");
+  return fn;
+}
+StreamValue32Fn write_value32() {
+  static StreamValue32Fn fn = stream_value32("cuStreamWriteValue32");
+  return fn;
+}
+// the multi-kernel paths' completion signal: a stream write after their last launch
+cudaError_t signal_call(const cm_graph* g, uint32_t seq, cudaStream_t st) {
+  StreamValue32Fn fn = write_value32();
+  if (!fn) return cudaErrorNotSupported;
+  return fn(st, reinterpret_cast<CUdeviceptr>(g->d_seq), seq, 0) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
+// Per-device function-attribute state (cudaFuncSetAttribute is per device): bit flags / sizes
+// indexed by device ordinal, under attr_mu.
+constexpr int kMaxDev = 64;
+std::mutex attr_mu;
+struct DevAttrs {
+  size_t scan_smem = 0;               // scan_kernel dynamic shared memory set so far
+  bool carve = false;                 // carve-out + K1 shared memory set
+  size_t v1_smem = 0;                 // row-form kernel
+};
+DevAttrs g_attrs[kMaxDev];
+
 EncodeTiledFn encode_tiled() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
@@ -144,9 +181,15 @@ struct Trace {
   std::vector<cudaEvent_t> ev;   // per chunk: k1 begin, k1 end, k2 begin, k2 end
   int used = 0;
 };
-Trace g_trace;
-uint64_t* g_cta_trace = nullptr;       // CM_TRACE=2: per-CTA timestamps of the last fused launch
-int32_t g_cta_trace_n = 0;
+// Debug state is per host thread (cm_debug_* report the calling thread's calls).
+thread_local Trace g_trace;
+// CM_TRACE=2: per-CTA timestamps of fused launches, kTraceCalls regions of 4 x kTraceCtas words
+// used in turn; the whole buffer is cleared when region 0 is reused, so consecutive calls
+// keep overlapping (no memset between them) for kTraceCalls - 1 calls
+constexpr int kTraceCalls = 16, kTraceCtas = 1024;
+thread_local uint64_t* g_cta_trace = nullptr;
+thread_local int32_t g_cta_trace_n = 0;
+thread_local int64_t g_cta_trace_calls = 0;   // fused calls traced so far by this thread
 thread_local int32_t g_launches = 0;   // kernels launched by this thread's last cm_round_and_evaluate
 bool trace_enabled() {
   const char* e = std::getenv("CM_TRACE");
@@ -265,12 +308,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       ? (tm ? reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>) : reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>))
       : (tm ? reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, true>) : reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>));
 
-  static std::mutex attr_mu;
-  static size_t set2 = 0;
+  DevAttrs& da = g_attrs[g->device];
   cudaError_t e;
   {
     std::lock_guard<std::mutex> lock(attr_mu);
-    if (smem2 > set2) {
+    if (smem2 > da.scan_smem) {
       for (const void* fn : {reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int64_t, false>),
                              reinterpret_cast<const void*>(cm2::scan_kernel<int32_t, true>),
@@ -279,7 +321,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                                  (int)std::max<size_t>(smem2, 48 * 1024));
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(scan_kernel)");
       }
-      set2 = smem2;
+      da.scan_smem = smem2;
     }
   }
   int occ1 = 0, occ2 = 0;
@@ -288,9 +330,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   auto smem1_for = [&](int nt) { return cm2::k1_smem_bytes(nt, nib_staged, bulk); };
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
-    static bool carve = false;
     std::lock_guard<std::mutex> lock(attr_mu);
-    if (!carve) {
+    if (!da.carve) {
       for (int nt = 1; nt <= 4; ++nt)
         for (int bl = 0; bl < 2; ++bl)
           for (int rd = 0; rd < 2; ++rd) {
@@ -309,7 +350,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "carveout(scan_kernel)");
       }
-      carve = true;
+      da.carve = true;
     }
   }
   const bool use_tma = a->layout == CM_LAYOUT_DENSE;
@@ -478,11 +519,19 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         fp.total_tasks = total_tasks;
         fp.win_units = (int32_t)win;
         fp.trace = nullptr;
-        if (env_flag("CM_TRACE", 0) == 2) {
-          if (!g_cta_trace) cudaMalloc(&g_cta_trace, 4 * sizeof(uint64_t) * 1024);
-          g_cta_trace_n = 4 * g->sm_count;
-          if (g_cta_trace) cudaMemsetAsync(g_cta_trace, 0, 4 * sizeof(uint64_t) * g->sm_count, st);
-          fp.trace = g_cta_trace;
+        if (env_flag("CM_TRACE", 0) == 2 && g->sm_count <= kTraceCtas) {
+          const size_t region = 4 * (size_t)kTraceCtas;
+          if (!g_cta_trace && cudaMalloc(&g_cta_trace, sizeof(uint64_t) * region * kTraceCalls) != cudaSuccess) {
+            g_cta_trace = nullptr;
+            cudaGetLastError();
+          }
+          if (g_cta_trace) {
+            const int64_t r = g_cta_trace_calls % kTraceCalls;
+            if (r == 0) cudaMemsetAsync(g_cta_trace, 0, sizeof(uint64_t) * region * kTraceCalls, st);
+            g_cta_trace_n = 4 * g->sm_count;
+            fp.trace = g_cta_trace + r * region;
+            ++g_cta_trace_calls;
+          }
         }
         {  // S* per producer ticket: 8 at n = 89, 2 at n = 213 .. ~420, 1 above
           const int gr = n >= 2 ? (n - 2) / 32 + 1 : 1;
@@ -500,13 +549,15 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           if (fp.task_claim < 1 || fp.tpu % fp.task_claim || win > 0) fp.task_claim = 1;
         }
         std::lock_guard<std::mutex> lock(g->mu);
+        fp.seq_word = g->d_seq;
+        fp.seq = ++g->seq;
         const int half = own_ws ? g->ws_half : 0;
         unsigned char* set_base = reinterpret_cast<unsigned char*>(ws) + half * set_bytes;
         uint32_t* ctl = reinterpret_cast<uint32_t*>(set_base);
         fp.ctl = ctl;
         fp.ring = reinterpret_cast<uint32_t*>(set_base + ctl_bytes(R));
         // (a call with a smaller ring left ring data where this call's control words lie)
-        if (!overlap || g->ctl_clean[half] < cm2::fused_ctl_words(R) || fp.trace) {
+        if (!overlap || g->ctl_clean[half] < cm2::fused_ctl_words(R)) {
           e = cudaMemsetAsync(ctl, 0, 4 * (size_t)cm2::fused_ctl_words(R), st);
           if (e != cudaSuccess) return cuda_fail(e, "memset(fused control words)");
         }
@@ -545,6 +596,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   const int64_t half = cap * cand_bytes(n, m32);
   std::lock_guard<std::mutex> lock(g->mu);
+  const uint32_t seq = ++g->seq;
   if (!a->workspace) g->ctl_clean[0] = g->ctl_clean[1] = 0;         // chunk buffers overwrite them
   const bool tr = trace_enabled();
   g_trace.used = 0;
@@ -624,6 +676,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     g->used[b] = true;
   }
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = signal_call(g, seq, st);
   if (e != cudaSuccess) return cuda_fail(e, "launch v2 kernels");
   return CM_OK;
 }
@@ -873,6 +926,8 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     g->ws_bytes = std::max<int64_t>(per * 1024, (want / (64 * per)) * 64 * per);
     e = cudaMalloc(&g->d_ws, g->ws_bytes);
   }
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_seq, 256);
+  if (e == cudaSuccess) e = cudaMemset(g->d_seq, 0, 256);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->st_round, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming);
   for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
@@ -885,6 +940,7 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     if (g->d_ws) cudaFree(g->d_ws);
     if (g->d_nib) cudaFree(g->d_nib);
     if (g->d_nib32) cudaFree(g->d_nib32);
+    if (g->d_seq) cudaFree(g->d_seq);
     cudaFree(g->d_blob);
     delete g;
     return fail(CM_ENOMEM, std::string("cm_graph_create: ") + cudaGetErrorString(e));
@@ -907,6 +963,7 @@ void cm_graph_destroy(cm_graph* g) {
   if (g->d_ws) cudaFree(g->d_ws);
   if (g->d_nib) cudaFree(g->d_nib);
   if (g->d_nib32) cudaFree(g->d_nib32);
+  if (g->d_seq) cudaFree(g->d_seq);
   delete g;
 }
 
@@ -926,11 +983,32 @@ int32_t cm_debug_trace(float* out, int32_t max_values) {
 
 int32_t cm_debug_last_launches(void) { return g_launches; }
 
-int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values) {
-  if (!g_cta_trace || !out) return 0;
+int32_t cm_debug_cta_trace_at(int32_t back, uint64_t* out, int32_t max_values) {
+  if (!g_cta_trace || !out || back < 0 || back >= kTraceCalls || back >= g_cta_trace_calls) return 0;
+  const int64_t r = (g_cta_trace_calls - 1 - back) % kTraceCalls;
   const int32_t m = std::min(max_values, g_cta_trace_n);
-  if (cudaMemcpy(out, g_cta_trace, sizeof(uint64_t) * (size_t)m, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  if (cudaMemcpy(out, g_cta_trace + r * 4 * (int64_t)kTraceCtas, sizeof(uint64_t) * (size_t)m,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
   return m;
+}
+
+int32_t cm_debug_cta_trace(uint64_t* out, int32_t max_values) { return cm_debug_cta_trace_at(0, out, max_values); }
+
+uint32_t cm_last_call_seq(const cm_graph* g) {
+  if (!g) return 0;
+  std::lock_guard<std::mutex> lock(const_cast<cm_graph*>(g)->mu);
+  return g->seq;
+}
+
+cm_status cm_stream_wait_call(const cm_graph* g, uint32_t seq, cm_stream stream) {
+  if (!g) return fail(CM_EINVAL, "NULL graph");
+  StreamValue32Fn fn = wait_value32();
+  if (!fn) return fail(CM_ECUDA, "cuStreamWaitValue32 unavailable");
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(g->d_seq), seq,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(CM_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+  return CM_OK;
 }
 
 cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const uint8_t* k_sets, float* sstar,
@@ -990,9 +1068,22 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   const int32_t idx_bits = cm_key_idx_bits(a->total_candidates);
   if (idx_bits > 62 || (idx_bits > 0 && g->cost_bound >= (int64_t(1) << (63 - idx_bits))))
     return fail(CM_ERANGE, "cost bound does not fit the packed key; use fewer candidates per key space");
+  {
+    int cur = -1;
+    const cudaError_t ed = cudaGetDevice(&cur);
+    if (ed != cudaSuccess) return cuda_fail(ed, "cudaGetDevice");
+    if (cur != g->device)
+      return fail(CM_EINVAL, "the graph lives on device " + std::to_string(g->device) + ", current device is " +
+                                 std::to_string(cur));
+    if (g->device >= kMaxDev) return fail(CM_ERANGE, "device ordinal >= 64");
+  }
   g_launches = 0;
   if (n_cand == 0) {
-    const cudaError_t e0 = init_keys(a, reinterpret_cast<cudaStream_t>(stream));
+    cm_graph* gm = const_cast<cm_graph*>(g);
+    std::lock_guard<std::mutex> lock(gm->mu);
+    const uint32_t seq = ++gm->seq;
+    cudaError_t e0 = init_keys(a, reinterpret_cast<cudaStream_t>(stream));
+    if (e0 == cudaSuccess) e0 = signal_call(g, seq, reinterpret_cast<cudaStream_t>(stream));
     return e0 == cudaSuccess ? CM_OK : cuda_fail(e0, "init keys");
   }
   if (kernel_choice() == 2 && (size_t)g->blob2_bytes + scan_warp_bytes(g->n_slot, g->scan32, false) <= (size_t)g->smem_optin) {
@@ -1020,15 +1111,14 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
 
   cudaError_t e = cudaGetLastError();                   // surface earlier asynchronous faults
   if (e != cudaSuccess) return cuda_fail(e, "earlier asynchronous error");
-  static std::mutex mu;
-  static size_t smem_set = 0;
   {
-    std::lock_guard<std::mutex> lock(mu);
-    if (smem > smem_set) {
+    std::lock_guard<std::mutex> lock(attr_mu);
+    DevAttrs& da = g_attrs[g->device];
+    if (smem > da.v1_smem) {
       e = cudaFuncSetAttribute(cmk::round_evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(smem, 48 * 1024));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-      smem_set = smem;
+      da.v1_smem = smem;
     }
   }
   int occ = 0;
@@ -1073,6 +1163,11 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   cmk::round_evaluate_kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(p);
   ++g_launches;
   e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    cm_graph* gm = const_cast<cm_graph*>(g);
+    std::lock_guard<std::mutex> lock(gm->mu);
+    e = signal_call(g, ++gm->seq, reinterpret_cast<cudaStream_t>(stream));
+  }
   if (e != cudaSuccess) return cuda_fail(e, "launch round_evaluate_kernel");
   return CM_OK;
 }

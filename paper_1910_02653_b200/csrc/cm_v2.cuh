@@ -1232,6 +1232,8 @@ struct FusedParams {
   int32_t win_units;          // ticket windows (units), 0: unit-major order
   uint64_t* trace;            // debug (CM_TRACE=2): per CTA {start, K1 end, ~first unit-0 task, K2 end} ns
   int32_t init_keys;          // CM_EVAL_INIT_KEYS: the first CTA sets the keys to INT64_MAX
+  uint32_t* seq_word;         // completion signal (cm_stream_wait_call): the last CTA out stores
+  uint32_t seq;               //   seq here once every output of the call is written
 };
 __host__ __device__ constexpr int64_t fused_ctl_words(int64_t R) { return 4 + 3 * R; }
 
@@ -1253,6 +1255,12 @@ __device__ __forceinline__ void fused_exit(const FusedParams& fp) {
     last = atomicAdd(fp.ctl + 2 + 3 * (int64_t)fp.n_slots, 1u) == gridDim.x - 1;
   }
   asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
+  if (last && threadIdx.x == 0 && fp.seq_word) {
+    // every CTA fenced its outputs before its exit count, and this CTA saw all the counts:
+    // publish the call's number to a stream wait on another stream (system-scope release)
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(fp.seq_word), "r"(fp.seq) : "memory");
+  }
   if (last) {
     __threadfence();
     for (int64_t i = threadIdx.x; i < words; i += blockDim.x) fp.ctl[i] = 0u;
