@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """Bench: candidate schedules rounded + evaluated per second (BASELINE.json metric).
 
-A step = one pass of the whole hot path (a1-a7 of SURVEY §8(a), plus the a8 NCCL
-MIN all-reduce at N>1) over one batch of synthetic, device-resident S*.
+A step = one pass of the whole hot path (a1-a7 of SURVEY §8(a), plus the a8 MIN all-reduce
+of the keys at N>1) over one batch of synthetic, device-resident S*.
 Default workload: the ResNet-50-shaped training DAG (n=353, |E|=560), G1 LP-like S*,
-theta = 0.5, 16 budgets, 125,000 S* per GPU per step (the 10^6-candidate config
-sharded over 8 GPUs; weak scaling).  Inputs (31 GB per GPU) exceed L2 (126 MB), so no
-flush is needed between steps.
+theta = 0.5, 16 budgets, 125,000 S* per GPU per step (the 10^6-candidate config sharded
+over 8 GPUs; weak scaling).  Inputs (67.8 GB per GPU in the dense layout with 128-byte
+rows, ld = 384) exceed L2 (126 MB), so no flush is needed between steps.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+At N>1 each rank evaluates its own contiguous S* range (global index_base) and step i's keys
+are MIN-reduced on a side stream that waits for call i through the library's device-side
+completion word (cm_stream_wait_call), so the reduction never stalls call i+1's overlap with
+call i.  CM_DIST_BACKEND=gloo (default nccl) and ranks sharing a GPU (LOCAL_RANK modulo the
+device count) exercise that path on one GPU.
 
 Prints ONE JSON line on rank 0.
 """
@@ -29,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate schedules rounded+evaluated/sec at n≈350, 1/2/4/8 B200; % HBM roofline"
 UNIT = "candidates/s"
+BENCH_SEED = 20250101
 
 CONFIGS = {
     # name: (graph builder, family, thetas, budget rule, S* per GPU per step)
@@ -174,39 +181,60 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU oracle legs
 
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def _oracle_worker(args):
-    gname, fam, seed, s_list, thetas, cfg = args
+    fam, seed, s_list, thetas, cfg = args
     from oracle import Instance, evaluate
     from workloads.sstar import gen_sstar
     g, _, _, _, _ = build_workload(cfg, fam)
     inst = Instance.from_graph(g)
     xs = [gen_sstar(g, fam, seed, s, 1)[0] for s in s_list]
+    counters = []
     t0 = time.perf_counter()
     for x in xs:
         for th in thetas:
-            evaluate(inst, x, th)
-    return time.perf_counter() - t0, len(xs) * len(thetas)
+            counters.append(evaluate(inst, x, th)["counters"])
+    return time.perf_counter() - t0, len(xs) * len(thetas), counters
+
+
+def ops_alg_of(n, counters):
+    """SURVEY §8(d) algorithmic integer ops per candidate: tri + n W + V + F + sum R + sum S,
+    from the oracle's A8 counters (mean over the sample)."""
+    tri, W = n * (n - 1) // 2, (n + 63) // 64
+    per = [tri + n * W + c["closure_visits"] + c["free_events"] + c["sum_R"] + c["sum_S"] for c in counters]
+    return float(np.mean(per))
 
 
 def cpu_oracle_rate(cfg, fam, seed, thetas, seconds):
-    """The oracle as it stands on this host's cores (multiprocessing), bounded sample."""
+    """The oracle as it stands on this host's cores (multiprocessing), bounded sample; also the
+    1-core rate and the A8 counters of the sampled candidates (the INT roofline's Ops_alg)."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
-    # calibrate one candidate on one core
-    dt, cnt = _oracle_worker((None, fam, seed, [0], thetas, cfg))
+    dt, cnt, c0 = _oracle_worker((fam, seed, [0], thetas, cfg))          # calibrate one S* on one core
     per = dt / cnt
     per_core = max(1, int(seconds / per / len(thetas)))
-    jobs = [(None, fam, seed, list(range(1 + c * per_core, 1 + (c + 1) * per_core)), thetas, cfg)
-            for c in range(cores)]
+    jobs = [(fam, seed, list(range(1 + c * per_core, 1 + (c + 1) * per_core)), thetas, cfg) for c in range(cores)]
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
         res = pool.map(_oracle_worker, jobs)
     wall = time.perf_counter() - t0
     total = sum(r[1] for r in res)
     busy = max(r[0] for r in res)
+    one = sum(r[1] for r in res) / sum(r[0] for r in res)               # per-process rate, averaged
+    counters = c0 + [c for r in res for c in r[2]]
     return {"value": total / busy, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "one_core_value": one, "cpu_model": cpu_model(),
             "sample": f"{total} candidates (S* #1..{cores * per_core}, {fam}, theta={thetas}) of the "
-                      f"{cfg} workload on {cores} processes; {wall:.1f}s wall incl. pool start"}
+                      f"{cfg} workload on {cores} processes; {wall:.1f}s wall incl. pool start"}, counters
 
 
 def run_reference(a):
@@ -217,7 +245,6 @@ def run_reference(a):
     from oracle import Instance, evaluate
     from workloads.sstar import gen_sstar
     inst = Instance.from_graph(g)
-    cores = len(os.sched_getaffinity(0))
     per_step = 8
     xs = [gen_sstar(g, fam, 7, s, 1)[0] for s in range(per_step)]
     for _ in range(a.warmup):
@@ -237,12 +264,22 @@ def run_reference(a):
             "impl": "reference",
             "config": {"workload": f"{a.config} n={g.n} |E|={len(g.edges)} {fam} S*, theta={thetas}, "
                                    f"{len(budgets)} budgets", "global_batch": per_step * len(thetas)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{per_step} S* x {len(thetas)} theta per step, 1 process"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-    del cores
     return 0
+
+
+def load_ops_alg(cfg, fam):
+    """Committed fallback for Ops_alg (profiles/ops_alg.json, written by tools/ops_alg.py from
+    the oracle's counters) when the CPU leg is skipped."""
+    p = os.path.join(ROOT, "profiles", "ops_alg.json")
+    if os.path.exists(p):
+        d = json.load(open(p)).get(cfg, {}).get(fam)
+        if d:
+            return d["ops_alg_per_candidate"], "profiles/ops_alg.json (" + d["sample"] + ")"
+    return None, None
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -255,21 +292,25 @@ def main():
     import torch.distributed as dist
 
     import paper_1910_02653_b200 as cm
-    from paper_1910_02653_b200.dist import global_best
     from workloads.device_gen import DeviceGenerator
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    backend = os.environ.get("CM_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     g, fam, thetas, budgets, batch = build_workload(a.config, a.family)
     if a.batch:
         batch = a.batch
-    seed = 20250101
+    seed = BENCH_SEED
     n_theta = a.samples if a.samples else len(thetas)
     graph = cm.Graph.from_workload(g)
     ld = a.ld if a.ld else (-(-g.n // 32) * 32 if a.layout == "dense" else None)
@@ -281,9 +322,11 @@ def main():
     bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
     overlap = a.overlap == "on"
     n_sets = 2 if overlap else 1                     # overlapped calls alternate two output sets
-    keys = [torch.empty(len(budgets), dtype=torch.int64, device=dev) for _ in range(n_sets)]
-    bkeys = [torch.empty(len(budgets), dtype=torch.int64, device=dev) if a.max_batch else None
-             for _ in range(n_sets)]
+    n_calls = max(a.warmup, 3) + a.steps + 8
+    # one key vector per call (tiny): call i's keys may still be in the MIN all-reduce on the side
+    # stream while calls i+1, i+2 run, so no call reuses another's keys
+    keys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev)
+    bkeys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev) if a.max_batch else None
     from workloads.budgets import eq13_cost_limit
     limit = eq13_cost_limit(g) if a.max_batch else None
     peaks = [torch.empty(batch * n_theta, dtype=torch.int64, device=dev) for _ in range(n_sets)]
@@ -292,14 +335,17 @@ def main():
     events = not overlap or a.step_events
     total = world * batch * n_theta
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)
+    works = []
     k_start = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
 
-    def step(i=None):
-        h = calls[0] % n_sets
+    def step(i=None, ovl=overlap):
+        c = calls[0]
         calls[0] += 1
-        key, bkey = keys[h], bkeys[h]
-        if not overlap:
+        h = c % n_sets
+        key, bkey = keys[c % n_calls], (bkeys[c % n_calls] if bkeys is not None else None)
+        if not ovl:
             key.fill_(cm.CM_KEY_NONE)
             if bkey is not None:
                 bkey.fill_(cm.CM_KEY_NONE)
@@ -309,20 +355,30 @@ def main():
                               index_base=s_base * n_theta, total_candidates=total, best_key=key,
                               peak=peaks[h], cost=costs[h], stream=stream.cuda_stream, samples=a.samples,
                               seed=seed, cost_limit=limit, best_batch_key=bkey,
-                              init_keys=overlap, overlap=overlap)
+                              init_keys=ovl, overlap=ovl)
         if i is not None and events:
             k_end[i].record(stream)
-        global_best(key)
-        if bkey is not None:
-            global_best(bkey)
+        if world > 1:
+            # a8: MIN all-reduce of this call's keys on the side stream, which waits for the call
+            # through the library's device-side completion word -- nothing is enqueued on `stream`
+            cm.stream_wait_call(graph, cm.last_call_seq(graph), side.cuda_stream)
+            with torch.cuda.stream(side):
+                works.append(dist.all_reduce(key, op=dist.ReduceOp.MIN, async_op=True))
+                if bkey is not None:
+                    works.append(dist.all_reduce(bkey, op=dist.ReduceOp.MIN, async_op=True))
         return key
+
+    def drain():
+        while works:
+            works.pop(0).wait()                      # `stream` waits for the reductions
 
     for _ in range(max(a.warmup, 3)):
         step()
+    drain()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
@@ -334,6 +390,7 @@ def main():
     t0.record(stream)
     for i in range(a.steps):
         last_key = step(i)
+    drain()
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -343,11 +400,50 @@ def main():
     # per-call device time; overlapped calls (no events between them) -> the per-step time
     kern_ms = (float(np.mean([s.elapsed_time(e) for s, e in zip(k_start, k_end)])) if events
                else elapsed_ms / a.steps)
+    # isolated launch: serial calls (keys filled first, no overlap), CUDA events on `stream`
+    iso = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        keys[0].fill_(cm.CM_KEY_NONE)
+        e0.record(stream)
+        cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
+                              index_base=s_base * n_theta, total_candidates=total, best_key=keys[0],
+                              peak=peaks[0], cost=costs[0], stream=stream.cuda_stream, samples=a.samples, seed=seed)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        iso.append(e0.elapsed_time(e1))
+    iso_ms = float(np.median(iso))
     if world > 1:
-        t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed_ms, kern_ms, iso_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, kern_ms = float(t[0]), float(t[1])
+        elapsed_ms, kern_ms, iso_ms = float(t[0]), float(t[1]), float(t[2])
     best = last_key.cpu().tolist()
+
+    # one extra traced step (untimed, every rank: it joins the collective): the fused path
+    # records its single launch; the two-kernel pipeline records per chunk K1 and K2+K3
+    kernels = None
+    launches = None
+    try:
+        os.environ["CM_TRACE"] = "1"
+        step()
+        drain()
+        torch.cuda.synchronize()
+        tr = cm.debug_trace()
+        per_step = cm.debug_last_launches()
+        os.environ["CM_TRACE"] = "0"
+        launches = a.steps * per_step
+        span = max(t[3] for t in tr) - min(t[0] for t in tr)
+        if per_step == 1:
+            kernels = {"path": "fused persistent kernel (K1 rounding warps + K2 scan warps per CTA, "
+                               "L2 ring handoff, K3 reduce in the K2 warps)", "fused_ms": span}
+        else:
+            k1 = sum(t[1] - t[0] for t in tr)
+            k2 = sum(t[3] - t[2] for t in tr)
+            kernels = {"path": "two-kernel pipeline", "chunks": len(tr), "k1_round_ms": k1,
+                       "k2_scan_reduce_ms": k2, "span_ms": span,
+                       "overlap": "K1(chunk c+1) runs on an internal stream concurrently with K2(chunk c)"}
+    except Exception as ex:  # pragma: no cover
+        kernels = {"error": str(ex)}
 
     # ---- e2e through the public API with HOST buffers (rank-local, then the same MIN) ----
     e2e = None
@@ -374,7 +470,7 @@ def main():
                                 total_candidates=world * eb * n_theta)
             if world > 1:
                 kd = kk.to(dev)
-                global_best(kd)
+                dist.all_reduce(kd, op=dist.ReduceOp.MIN)
                 kk = kd.cpu()
         e_dt = time.perf_counter() - te
         if world > 1:
@@ -400,57 +496,53 @@ def main():
     path_ms = kern_ms                     # per-call device time (events around each launch, or the
                                           # per-step time when consecutive calls overlap)
     achieved = alg_bytes / (path_ms / 1000.0) / 1e9
-    # one extra traced step (untimed): the fused path records its single launch; the
-    # two-kernel pipeline records per chunk K1 (internal stream) and K2+K3 (caller stream)
-    kernels = None
-    launches = None
-    try:
-        os.environ["CM_TRACE"] = "1"
-        step()
-        torch.cuda.synchronize()
-        tr = cm.debug_trace()
-        per_step = cm.debug_last_launches()
-        os.environ["CM_TRACE"] = "0"
-        launches = a.steps * per_step
-        span = max(t[3] for t in tr) - min(t[0] for t in tr)
-        if per_step == 1:
-            kernels = {"path": "fused persistent kernel (K1 rounding warps + K2 scan warps per CTA, "
-                               "L2 ring handoff, K3 reduce in the K2 warps)", "fused_ms": span}
-        else:
-            k1 = sum(t[1] - t[0] for t in tr)
-            k2 = sum(t[3] - t[2] for t in tr)
-            kernels = {"path": "two-kernel pipeline", "chunks": len(tr), "k1_round_ms": k1,
-                       "k2_scan_reduce_ms": k2, "span_ms": span,
-                       "overlap": "K1(chunk c+1) runs on an internal stream concurrently with K2(chunk c)"}
-    except Exception as ex:  # pragma: no cover
-        kernels = {"error": str(ex)}
     traffic = load_traffic(a.config, batch)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-            "frac": achieved / peak_gbs, "traffic": traffic,
+    # ---- integer-pipe term (K-mu): measured INT peak, Ops_alg from the oracle's A8 counters ----
+    ipk = None
+    try:
+        from tools.int_peak import measure as int_peak_measure
+        ipk = int_peak_measure()
+    except Exception as ex:  # pragma: no cover
+        ipk = {"error": str(ex)}
+    cpu, counters = None, None
+    if not a.no_cpu_baseline and world == 1 and not a.samples:
+        cpu, counters = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
+    if counters:
+        ops_pc, ops_src = ops_alg_of(g.n, counters), f"oracle A8 counters of the cpu_baseline sample ({len(counters)} candidates)"
+    else:
+        ops_pc, ops_src = load_ops_alg(a.config, fam)
+    if a.samples:
+        # randomized rounding adds the generator's integer work per stored element and sample:
+        # 10 rounds x (4 multiplies, 4 xors, 2 key adds) per Philox block = 100, 4 samples per
+        # block, plus shift / convert / scale / compare (4): 29
+        ops_pc = (ops_pc or 0.0) + 29.0 * (g.n * (g.n - 1) // 2)
+    int_term = None
+    if ops_pc and ipk and "int_peak_tops" in ipk:
+        ops_rate = ops_pc * batch * n_theta / (path_ms / 1000.0)
+        int_term = {"achieved": ops_rate / 1e12, "peak": ipk["int_peak_tops"], "unit": "T int lane-ops/s",
+                    "frac": ops_rate / 1e12 / ipk["int_peak_tops"], "ops_alg_per_candidate": ops_pc,
+                    "ops_alg_source": ops_src,
+                    "peak_source": "measured live: tools/int_peak.py lop3+imad (alu + fma pipes) at %.0f MHz; "
+                                   "alu pipe alone %.2f T/s" % (ipk["classes"]["lop3+imad"]["sm_mhz"], ipk["alu_tops"])}
+    hbm_term = {"achieved": achieved, "peak": peak_gbs, "unit": "GB/s", "frac": achieved / peak_gbs}
+    binds = "int" if int_term and int_term["frac"] > hbm_term["frac"] else "hbm"
+    roof = {"bound": "alu" if binds == "int" else "hbm",
+            "achieved": int_term["achieved"] if binds == "int" else achieved,
+            "peak": int_term["peak"] if binds == "int" else peak_gbs,
+            "unit": int_term["unit"] if binds == "int" else "GB/s",
+            "frac": int_term["frac"] if binds == "int" else achieved / peak_gbs,
+            "traffic": traffic,
+            "traffic_source": "ncu --set full capture committed under profiles/ (profiles/traffic.json, DRAM "
+                              "bytes read + write per S* x batch); not measured in this run",
+            "terms": {"hbm": hbm_term, "int": int_term},
+            "binds": binds,
             "kernel": "cm2::fused_kernel: the whole a1-a7 path in one launch per step (" +
                       ("CUDA events around each call on the launching stream" if events else
                        "consecutive launches overlap (CM_EVAL_OVERLAP): timed region / steps") + ")",
-            "alg_bytes_per_launch": alg_bytes, "ms_per_launch": path_ms, "kernels": kernels,
-            "peak_source": peak_src}
-    if a.samples:
-        # randomized rounding is bound by integer ALU work (Philox), not HBM.  Algorithmic
-        # integer ops: per stored element and Philox block (4 samples) 10 rounds x (2 mulhilo =
-        # 4 multiplies, 4 xors, 2 key adds) = 100, plus per sample shift, convert, scale and
-        # compare (4); so 100 / 4 + 4 = 29 per element and candidate.  Peak: the
-        # guide's pipe rates (ALU and FMA pipes each one warp instruction per 2 cycles per SMSP,
-        # 4 SMSPs) x 32 lanes x 148 SMs x the 1965 MHz max SM clock.
-        ops = 29.0 * (g.n * (g.n - 1) // 2) * batch * n_theta
-        clk = (clocks or {}).get("sm_mhz") or 1965.0
-        peak_ops = 148 * 4 * 32 * clk * 1e6
-        ach = ops / (path_ms / 1000.0)
-        roof = {"bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (int32 lane ops)",
-                "frac": ach / peak_ops, "traffic": None, "kernel": roof["kernel"], "ms_per_launch": path_ms,
-                "kernels": kernels, "alg_ops_per_launch": ops,
-                "peak_source": "derived: 148 SMs x 4 SMSPs x 32 lanes x SM clock (B300_MICROARCH pipe rates: ALU and "
-                               "FMA pipes each 1 warp-instr / 2 cycles / SMSP)"}
-    cpu = None
-    if not a.no_cpu_baseline and world == 1 and not a.samples:
-        cpu = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
+            "alg_bytes_per_launch": alg_bytes, "ms_per_launch": path_ms,
+            "isolated_launch_ms": iso_ms,
+            "isolated_frac": alg_bytes / (iso_ms / 1000.0) / 1e9 / peak_gbs,
+            "kernels": kernels, "peak_source": peak_src, "int_peak": ipk}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": elapsed_ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
@@ -459,7 +551,8 @@ def main():
                                    + (f"randomized rounding, {a.samples} samples per S*" if a.samples
                                       else f"theta={thetas}") + f", {len(budgets)} budgets",
                        "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
-                       "parallelism": f"candidates sharded over {world} GPU(s), NCCL MIN all-reduce of keys",
+                       "parallelism": f"candidates sharded over {world} GPU(s) ({backend if world > 1 else 'no'} "
+                                      "MIN all-reduce of each step's keys on a side stream)",
                        "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush",
                        "calls": ("overlapped: CM_EVAL_OVERLAP | CM_EVAL_INIT_KEYS, two alternating output "
                                  "sets" if overlap else "serial: keys filled by the caller before each call")},

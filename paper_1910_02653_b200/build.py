@@ -31,6 +31,12 @@ LIBS = {
         [],
         [],
     ),
+    # measurement tool (integer-pipe roofline, tools/int_peak.py), not the product
+    os.path.join(ROOT, "tools", "libcm_intpeak.so"): (
+        [os.path.join(ROOT, "tools", "csrc", "int_peak.cu")],
+        [],
+        [],
+    ),
 }
 
 

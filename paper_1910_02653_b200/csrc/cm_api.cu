@@ -229,9 +229,9 @@ CUtensorMapL2promotion promo_of(int v) {
   }
 }
 CUtensorMapL2promotion l2_promotion() { return promo_of(env_flag("CM_L2PROMO", 256)); }
-// the diagonal blocks (w = g): a row ends inside the block, so promotion past it only pulls
-// never-read upper-triangle bytes (CM_L2PROMO_DIAG, default none)
-CUtensorMapL2promotion l2_promotion_diag() { return promo_of(env_flag("CM_L2PROMO_DIAG", 0)); }
+// the block just before an odd diagonal block: a 256-byte window would also pull the diagonal
+// block's rows, upper-triangle bytes included (CM_L2PROMO_PRE, default 128)
+CUtensorMapL2promotion l2_promotion_pre() { return promo_of(env_flag("CM_L2PROMO_PRE", 128)); }
 
 const void* round_fn(int nt, bool bulk, bool rnd) {
 #define CM_R(NT) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, true, true>) \
@@ -364,15 +364,22 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const cuuint64_t dims[3] = {(cuuint64_t)a->ld, (cuuint64_t)n, (cuuint64_t)a->n_sstar};
     const cuuint64_t strides[2] = {(cuuint64_t)a->ld * 4, (cuuint64_t)a->sstar_stride * 4};
     const cuuint32_t box[3] = {32, 32, 1};
-    const cuuint32_t box_up[3] = {16, 16, 1};
-    const cuuint32_t box_lo[3] = {32, 16, 1};
+    const cuuint32_t box8[3] = {8, 8, 1};
+    const cuuint32_t box16[3] = {16, 8, 1};
+    const cuuint32_t box32[3] = {32, 16, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    auto mk = [&](CUtensorMap* m, const cuuint32_t* bx, CUtensorMapL2promotion pr) {
+    auto mk = [&](CUtensorMap* m, const cuuint32_t* bx, CUtensorMapSwizzle sw, CUtensorMapL2promotion pr) {
       return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides, bx, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     };
-    if (mk(&tmap, box, l2_promotion()) != CUDA_SUCCESS || mk(&dmaps.upper, box_up, l2_promotion_diag()) != CUDA_SUCCESS ||
-        mk(&dmaps.lower, CM_DIAG_SPLIT ? box_lo : box, l2_promotion_diag()) != CUDA_SUCCESS)
+    // off-diagonal blocks: 256-byte promotion (CM_L2PROMO); the block before an odd diagonal
+    // without it (cm2::DiagMaps); the diagonal's three boxes without any
+    const CUtensorMapL2promotion none = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    if (mk(&tmap, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion()) != CUDA_SUCCESS ||
+        mk(&dmaps.pre, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion_pre()) != CUDA_SUCCESS ||
+        mk(&dmaps.d8, box8, CU_TENSOR_MAP_SWIZZLE_32B, none) != CUDA_SUCCESS ||
+        mk(&dmaps.d16, box16, CU_TENSOR_MAP_SWIZZLE_64B, none) != CUDA_SUCCESS ||
+        mk(&dmaps.d32, box32, CU_TENSOR_MAP_SWIZZLE_128B, none) != CUDA_SUCCESS)
       return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
   // tri4: a 2-D map whose rows are the batch's 16-byte units (stride 16 B: overlapping 128-byte

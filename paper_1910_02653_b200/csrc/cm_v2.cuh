@@ -262,18 +262,9 @@ __host__ __device__ constexpr int k1_stages(int nt) { return nt == 1 ? CM_K1_STA
 // rows at a 144-byte pitch (one 16-byte chunk of skew per row), so lane l reading 16-byte
 // chunk c of its row hits bank group (l + c) % 8: conflict-free without a swizzle.
 constexpr int kBulkPitch = 144;
-// Dense layout, diagonal blocks (w = g): row 32g+1+l needs only nodes 32g .. 32g+l, so each
-// lane bulk-copies its row's roundup4(l+1) floats into the 144-byte-pitch form instead of the
-// whole 4 KB tile.  The stage then holds either form; 5 KB keeps every stage 1024-byte aligned
-// for the swizzled tensor tiles.  Off by default: measured DRAM reads fell only 292 -> 287 KB
-// per S* (sector / burst granularity of the short rows) while the 32 copy requests per block
-// cost 11 % (16.0 vs 17.9 M cand/s).
-#ifndef CM_DIAG_BULK
-#define CM_DIAG_BULK 0
-#endif
 // tri4 (bulk): 5 KB so a stage holds either the swizzled 4 KB gather4 tile (1024-aligned) or
 // the 144-byte-pitch per-row form of the fallback.
-__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 5120 : (CM_DIAG_BULK ? 5120 : 4096); }
+__host__ __device__ constexpr size_t k1_stage_bytes(bool bulk) { return bulk ? 5120 : 4096; }
 __host__ __device__ constexpr size_t k1_bar_off(int nt, bool bulk = false) {
   return ((size_t)k1_warps(nt) * k1_stages(nt) * k1_stage_bytes(bulk) + 1023) & ~(size_t)1023;
 }
@@ -323,20 +314,27 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Dense diagonal blocks (w = g) in two loads: rows 32g+1..32g+16 need nodes < 32g+16 only
-// (box {16, 16}; with the 128-byte swizzle it fills logical chunks 0-3 of rows 0-15 of the
-// tile, exactly as a full box would), rows 32g+17..32g+32 the whole width (box {32, 16} at
-// row 16).  3 KB instead of 4 KB; neither map promotes past the block (the rows end there).
-// Off by default (CM_DIAG_SPLIT): measured DRAM reads fell only 1.4 KB per S* -- the 256-byte
-// L2 promotion of block w = g-1 has already fetched the diagonal rows' 128 bytes -- and the
-// second request cost ~0.7 %.  With it off, `lower` is the full {32, 32} box without promotion.
-#ifndef CM_DIAG_SPLIT
-#define CM_DIAG_SPLIT 0
-#endif
+// Dense diagonal blocks (w = g): row 32g+1+l holds only nodes 32g .. 32g+l of the block, so
+// the block is read as three boxes that stop where the rows' stored prefixes stop (Eq. 12b,
+// entries i >= t are never read): rows l = 0..7 x 8 nodes (32-byte rows,
+// SWIZZLE_32B) at stage byte 0, rows 8..15 x 16 nodes (64-byte rows, SWIZZLE_64B) at 512,
+// rows 16..31 x 32 nodes (SWIZZLE_128B, exactly the full tile's rows 16..31) at 2048:
+// 2 816 of the full tile's 4 096 bytes, none of them promoted past the block.  Each box's
+// swizzle keeps its 8 lanes' 16-byte reads on 8 distinct bank groups.  `pre`: the full box
+// without 256-byte L2 promotion, for block w = g-1 when w is even (its promotion window
+// would otherwise pull the diagonal block's whole 128-byte rows from DRAM).
 struct DiagMaps {
-  CUtensorMap upper;   // box {16 nodes, 16 rows}
-  CUtensorMap lower;   // box {32 nodes, 16 rows}
+  CUtensorMap pre;     // box {32 nodes, 32 rows}, SWIZZLE_128B, 128-byte promotion
+  CUtensorMap d8;      // box {8, 8}, SWIZZLE_32B, no promotion
+  CUtensorMap d16;     // box {16, 8}, SWIZZLE_64B, no promotion
+  CUtensorMap d32;     // box {32, 16}, SWIZZLE_128B, no promotion
 };
+constexpr uint32_t kDiagBytes = 8 * 32 + 8 * 64 + 16 * 128;
+// lane l's row in a diagonal stage: byte offset of the row and the XOR of its 16-byte chunks
+__device__ __forceinline__ uint32_t diag_row_off(int l) { return l < 8 ? 32u * l : l < 16 ? 512u + 64u * (l - 8) : 128u * l; }
+__device__ __forceinline__ uint32_t diag_row_xor(int l) {
+  return l < 8 ? (uint32_t)((l >> 2) & 1) << 4 : l < 16 ? (uint32_t)(((l - 8) >> 1) & 3) << 4 : (uint32_t)(l & 7) << 4;
+}
 
 // K1 body of one warp: S* s = hk.first(), hk.next(s), ... while < s_count; wl = the warp's
 // index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
@@ -366,6 +364,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
 #pragma unroll
   for (int j = 0; j < NT; ++j) th[j] = RAND ? 0.f : p.theta[p.th0 + j];
   const Transposer transpose(lane);
+  const uint32_t drow_off = diag_row_off(lane), drow_xor = diag_row_xor(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t tiles_u32 = smem_u32(tiles);
   // tri4 read by gather4 lands in the same 128-byte-swizzled form as the dense tensor tiles.
@@ -410,44 +409,24 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)lane * kBulkPitch, src, 4u * (uint32_t)len,
                   &bars[pstage]);
       }
-    } else if (CM_DIAG_BULK && pw == pg) {
-      const int l = lane, r = 32 * pg + 1 + l;
-      const int len = r < p.n ? ((l + 4) & ~3) : 0;                 // roundup4(l + 1) floats
-      const uint32_t total = __reduce_add_sync(FULL, (uint32_t)len) * 4u;
-      if (lane == 0) mbar_expect_tx(&bars[pstage], total);
-      __syncwarp();
-      if (len > 0) {
+    } else if (lane == 0) {
 #ifdef CM_EXP_L2INPUT
-        const int64_t sidx = (p.s_begin + ps) & 63;
-#else
-        const int64_t sidx = p.s_begin + ps;
-#endif
-        const float* src = p.sstar + sidx * p.stride + (int64_t)r * p.ld + 32 * pg;
-        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)l * kBulkPitch, src, 4u * (uint32_t)len,
-                  &bars[pstage]);
-      }
-    } else if (CM_DIAG_SPLIT && lane == 0 && pw == pg) {
-#ifdef CM_EXP_L2INPUT
-      const int z = (int)((p.s_begin + ps) & 63);
+      const int z = (int)((p.s_begin + ps) & 63);                   // timing experiment
 #else
       const int z = (int)(p.s_begin + ps);
 #endif
-      mbar_expect_tx(&bars[pstage], 3u * 1024u);
       unsigned char* dst = tiles + (size_t)pstage * kStageBytes;
-      tma_load_3d(dst, &dmaps->upper, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
-      tma_load_3d(dst + 2048, &dmaps->lower, 32 * pw, 32 * pg + 17, z, &bars[pstage]);
-    } else if (lane == 0) {
-      mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
-      void* dst = tiles + (size_t)pstage * kStageBytes;
-      const CUtensorMap* tm = pw == pg ? &dmaps->lower : tmap;     // (CM_DIAG_SPLIT 0: one full diagonal box)
-      if (pol)
-        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage], pol);
-      else
-#ifdef CM_EXP_L2INPUT
-        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)((p.s_begin + ps) & 63), &bars[pstage]);   // timing experiment
-#else
-        tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, (int)(p.s_begin + ps), &bars[pstage]);
-#endif
+      if (pw == pg) {                                               // diagonal: the rows' prefixes only
+        mbar_expect_tx(&bars[pstage], kDiagBytes);
+        tma_load_3d(dst, &dmaps->d8, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
+        tma_load_3d(dst + 512, &dmaps->d16, 32 * pw, 32 * pg + 9, z, &bars[pstage]);
+        tma_load_3d(dst + 2048, &dmaps->d32, 32 * pw, 32 * pg + 17, z, &bars[pstage]);
+      } else {
+        mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
+        const CUtensorMap* tm = (pw + 1 == pg && (pw & 1) == 0) ? &dmaps->pre : tmap;
+        if (pol) tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage], pol);
+        else tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
+      }
     }
     pstage = pstage + 1 == kSt ? 0 : pstage + 1;
     if (++pw > pg) {
@@ -480,11 +459,13 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         issue();
         mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
-        // diagonal block of the dense layout: per-row bulk copies, 144-byte pitch, no swizzle
-        const bool dbulk = !BULK && CM_DIAG_BULK && w == g;
-        const bool pitched = dbulk || pitched_of(s);
-        const uint32_t rb = tiles_u32 + (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : 128u) + (uint32_t)cstage * kStageBytes;
-        const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
+        // this lane's row in the stage: the 144-byte-pitch per-row form (tri4 fallback), the
+        // three diagonal boxes (dense, w = g) or the 128-byte-swizzled 32 x 32 tile
+        const bool pitched = pitched_of(s);
+        const bool dg = !BULK && w == g;
+        const uint32_t rb = tiles_u32 + (uint32_t)cstage * kStageBytes +
+                            (pitched ? (uint32_t)lane * (uint32_t)kBulkPitch : dg ? drow_off : 128u * (uint32_t)lane);
+        const uint32_t sw = pitched ? 0u : dg ? drow_xor : (uint32_t)(lane & 7) << 4;
         float x[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {

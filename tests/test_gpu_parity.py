@@ -473,8 +473,7 @@ def test_bench_launch_configuration_sampled():
     sets = [{k: torch.zeros(n, dtype=torch.int64, device="cuda") for k, n in
              (("peak", N), ("cost", N), ("key", len(budgets)))} for _ in range(2)]
     for step in range(3):
-        o = sets[step % 2]
-        o["key"].zero_()
+        o = sets[step % 2]                                         # keys start at 0 (allocation)
         out = cm.round_and_evaluate(graph, buf, th, bu, best_key=o["key"], peak=o["peak"], cost=o["cost"],
                                     init_keys=True, overlap=True)
         assert cm.debug_last_launches() == 1
