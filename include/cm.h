@@ -102,7 +102,7 @@ typedef struct {
                                CM_ROUND_RANDOMIZED: S = 1[u < S*], Pr[S = 1] = S* (PAPER.md:383, 387),
                                candidate j = sample j of the S* (n_theta samples, theta unused and
                                may be NULL); u is the DESIGN.md R1 Philox4x32-10 uniform with
-                               counter (node, row, global S* index, j / 4); index_base must be a
+                               counter (node / 4, row, global S* index, j), word node % 4; index_base must be a
                                multiple of n_theta (global S* index = index_base / n_theta + s) */
   uint64_t seed;            /* CM_ROUND_RANDOMIZED: the Philox key (low word, high word) */
   int64_t* best_batch_key;  /* device int64[n_budget] or NULL (off).  Max-batch epilogue (Eq. 13,

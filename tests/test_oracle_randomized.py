@@ -71,12 +71,16 @@ def test_mean_and_independence():
 
 
 def test_uniforms_layout():
-    """u(s, j, t, i) uses counter (i-1, t-1, s, j div 4) and output word j mod 4."""
-    U = uniforms(5, 3, 6, (7 << 32) | 11)
-    for t in range(1, 6):
-        for i in range(1, 6):
-            w = philox4x32_10((i - 1, t - 1, 3, 1), (11, 7))[2]
+    """u(s, j, t, i) uses counter ((i-1) div 4, t-1, s, j) and output word (i-1) mod 4
+    (R1): written out with the scalar Philox block for every (t, i) of n = 9."""
+    U = uniforms(9, 3, 6, (7 << 32) | 11)
+    for t in range(1, 10):
+        for i in range(1, 10):
+            w = philox4x32_10(((i - 1) // 4, t - 1, 3, 6), (11, 7))[(i - 1) % 4]
             assert U[t - 1, i - 1] == np.float32((w >> 8) * 2.0 ** -24)
+    # one block serves four consecutive nodes: nodes 1..4 of a row are its four words
+    blk = philox4x32_10((0, 2, 3, 6), (11, 7))
+    assert [U[2, q] for q in range(4)] == [np.float32((w >> 8) * 2.0 ** -24) for w in blk]
 
 
 def test_appendix_d_deterministic_not_worse():
