@@ -513,8 +513,8 @@ def main():
         ops_pc, ops_src = load_ops_alg(a.config, fam)
     if a.samples:
         # randomized rounding adds the generator's integer work per stored element and sample:
-        # 10 rounds x (4 multiplies, 4 xors, 2 key adds) per Philox block = 100, 4 samples per
-        # block, plus shift / convert / scale / compare (4): 29
+        # 10 rounds x (4 multiplies, 4 xors, 2 key adds) per Philox block = 100, one block per
+        # four (node, sample) uniforms (R1), plus scale / convert / compare (4): 29
         ops_pc = (ops_pc or 0.0) + 29.0 * (g.n * (g.n - 1) // 2)
     int_term = None
     if ops_pc and ipk and "int_peak_tops" in ipk:

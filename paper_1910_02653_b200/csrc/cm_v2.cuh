@@ -13,7 +13,7 @@
 //       Sn_g[i]  bit b = S_{row 32g+b+1, node i} = S_{t+1}   for stage t = 32g+b+1,
 //   i.e. the NEXT stage's checkpoint bits (S_{n+1} = 0).  The current stage's
 //   bits follow from them and row 32g's word (brow).  One S* read serves up to 4 thresholds
-//   (or 4 random samples, RAND: Philox4x32-10, R1).
+//   (or 4 random samples, RAND: Philox4x32-10, one block per 4 nodes and sample, R1).
 //
 // K2 task (scan_task; latency / ALU-bound), per (group g, 32 candidates): one pass over nodes
 //   k = nk-1 .. 0 (reverse topological order, the paper's right-to-left scan):
@@ -133,7 +133,7 @@ struct RoundParams {
   int32_t brow;               // word offset of brow in a candidate block
   int32_t evict_first;        // S* loads with an L2 evict-first policy
   // randomized rounding (R1): S = u < S*, u from Philox4x32-10 with counter
-  // (node, row, global S* index, sample / 4) and key (key0, key1); sample j = th0 + j
+  // (node / 4, row, global S* index, sample) and key (key0, key1), word node % 4; sample j = th0 + j
   uint32_t key0, key1;
   uint32_t s0;                // global index of batch S* 0 (mod 2^32)
   int32_t g4;                 // tri4: tile::gather4 through the 16-byte-unit tensor map (else per-row copies)
@@ -341,7 +341,7 @@ __device__ __forceinline__ uint32_t diag_row_xor(int l) {
 // consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
 // takes queue in `sq` (8 per warp) until the consumer reaches them.
 // RAND: randomized rounding, sample th0 + j instead of threshold th0 + j (one Philox block
-// gives the four samples of a pass).
+// per four consecutive nodes and sample).
 template <int NT, bool BULK, bool RAND, class Hooks>
 __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const DiagMaps* dmaps,
                                         unsigned char* k1smem,
@@ -482,29 +482,34 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         const uint32_t rmask = rq >= p.n ? 0u : (rem >= 32 ? FULL : (1u << rem) - 1u);
         uint32_t word[NT];
         if (RAND) {                                                 // a1 randomized: u < S*
+          // DESIGN.md R1: sample th0 + j of node i-1 = 32w + q in row rq is word q % 4 of the
+          // Philox block with counter (8w + q / 4, rq, global S* index, th0 + j): one block per
+          // four consecutive nodes and sample
           uint32_t rw[NT];
 #pragma unroll
           for (int j = 0; j < NT; ++j) rw[j] = 0u;
           const uint32_t sg = p.s0 + (uint32_t)(p.s_begin + s);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const uint4 o = philox4x32_10(make_uint4((uint32_t)(32 * w + q), (uint32_t)rq, sg, (uint32_t)(p.th0 >> 2)),
-                                          p.key0, p.key1);
-            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-            // u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < ceil(x 2^24): the scaling is exact in fp32,
-            // t is clamped to [0, 2^24] (x > 1 or inf: always; x <= 0: never) and NaN converts to 0
-            const float xs = x[q] * 16777216.0f;
-            const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
-            if (NT >= 2) {
-              // (w >> 8) < t  <=>  w <= 256 t - 1 for t >= 1 (t = 2^24 wraps to 2^32 - 1:
-              // always); t = 0: never.  One compare per sample instead of shift + compare
-              // (measured 4 samples 8.70 vs 8.57 M cand/s; 1 sample: slower, kept below)
-              const uint32_t tw = (t << 8) - 1u;
-              const uint32_t qb = t != 0u ? (1u << q) : 0u;
+          for (int q4 = 0; q4 < 8; ++q4) {
+            // u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < t = ceil(x 2^24) (exact in fp32; t clamped
+            // to [0, 2^24]: x > 1 or inf always, x <= 0 or NaN never)  <=>  w <= 256 t - 1 for
+            // t >= 1 (t = 2^24 wraps to 2^32 - 1: always); t = 0: never
+            uint32_t tw[4], qb[4];
 #pragma unroll
-              for (int j = 0; j < NT; ++j) rw[j] |= ow[j] <= tw ? qb : 0u;
-            } else {
-              rw[0] |= (ow[0] >> 8) < t ? (1u << q) : 0u;
+            for (int e = 0; e < 4; ++e) {
+              const int q = 4 * q4 + e;
+              const float xs = x[q] * 16777216.0f;
+              const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
+              tw[e] = (t << 8) - 1u;
+              qb[e] = t != 0u ? (1u << q) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
+                                            p.key0, p.key1);
+              const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) rw[j] |= ow[e] <= tw[e] ? qb[e] : 0u;
             }
           }
 #pragma unroll
