@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--samples", type=int, default=None,
                     help="randomized rounding (DESIGN.md R1) with this many samples per S* instead of the thresholds")
     ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
-    ap.add_argument("--layout", default="dense", choices=["tri4", "dense"])
+    ap.add_argument("--layout", default="dense", choices=["tri4", "dense", "blk"])
     ap.add_argument("--ld", type=int, default=None,
                     help="dense row stride in floats (default: n rounded up to 32, i.e. 128-byte rows)")
     ap.add_argument("--overlap", default="on", choices=["on", "off"],

@@ -46,6 +46,17 @@ typedef enum {
 #define CM_EMAX 8192          /* max edges */
 #define CM_LAYOUT_DENSE 0     /* S* row r at sstar + r*ld, ld >= n, ld % 4 == 0 */
 #define CM_LAYOUT_TRI4 1      /* S* row r at sstar + sum_{r'<r} roundup4(r') (packed strict lower triangle) */
+#define CM_LAYOUT_BLK 2       /* blocked strict lower triangle (the layout the kernel reads in one copy per
+                                 32 x 32 block; 0.85 % over the triangle's bytes at n = 353):
+                                 row group g = rows 32g+1 .. 32g+h_g, h_g = min(32, n-1-32g), g = 0..Gr-1,
+                                 Gr = ceil((n-1)/32); blocks w = 0..g (nodes 32w .. 32w+31) stored group
+                                 after group, block after block, block (g, w) at float offset
+                                 4 (128 g (g-1) + 144 g) + 32 h_g w.  Off-diagonal block (w < g): h_g rows
+                                 x 32 floats, the 4-float chunk c of row l (nodes 32w+4c ..) at chunk
+                                 c XOR (l mod 8).  Diagonal block (w = g): chunk-major, chunk c of rows
+                                 l = 4c .. h_g-1 at chunk B_c + l - 4c, B_c = sum_{c'<c} max(0, h_g - 4c').
+                                 Entries with i >= t inside a stored chunk are never read.
+                                 cm_sstar_floats gives the size. */
 #define CM_KEY_NONE INT64_MAX /* best_key value meaning "no feasible candidate" */
 #define CM_ROUND_THRESHOLD 0  /* cm_eval_args.rounding: deterministic threshold rounding */
 #define CM_ROUND_RANDOMIZED 1 /* cm_eval_args.rounding: randomized rounding (R1) */
@@ -77,10 +88,10 @@ int64_t cm_graph_cost_bound(const cm_graph* g); /* sum_i (n-i) C_i: an upper bou
 
 typedef struct {
   int32_t n_sstar;          /* number of S* matrices in this call, >= 0 */
-  int32_t layout;           /* CM_LAYOUT_DENSE or CM_LAYOUT_TRI4 */
+  int32_t layout;           /* CM_LAYOUT_DENSE, CM_LAYOUT_TRI4 or CM_LAYOUT_BLK */
   const float* sstar;       /* device, 16-byte aligned; only entries i < t of row t are read (Eq. 12b) */
   int64_t ld;               /* dense: row stride in floats, ld >= n, ld % 4 == 0; tri4: ignored */
-  int64_t sstar_stride;     /* floats between consecutive S*, % 4 == 0; >= n*ld (dense) / tri4 size */
+  int64_t sstar_stride;     /* floats between consecutive S*, % 4 == 0; >= cm_sstar_floats(n, layout, ld) */
   int32_t n_theta;          /* >= 1 */
   const float* theta;       /* device fp32[n_theta]; rule S = S* > theta, NaN -> 0 (Q1, Q6) */
   int32_t n_budget;         /* >= 0 */
@@ -155,6 +166,10 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* args, cm_
  */
 uint32_t cm_last_call_seq(const cm_graph* g);
 cm_status cm_stream_wait_call(const cm_graph* g, uint32_t seq, cm_stream stream);
+
+/* Floats one S* occupies in `layout` (dense: n * ld, ld >= n); the minimum sstar_stride.  -1 for a
+ * bad layout / n < 1 / ld < n.  Host function. */
+int64_t cm_sstar_floats(int32_t n, int32_t layout, int64_t ld);
 
 /* Bytes of workspace needed to process `chunk_candidates` candidates per internal chunk
  * (the library splits a batch into chunks that fit the workspace it is given). */

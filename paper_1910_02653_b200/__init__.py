@@ -12,7 +12,8 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (CM_EMAX, CM_KEY_NONE, CM_LAYOUT_DENSE, CM_LAYOUT_TRI4, CM_ROUND_RANDOMIZED,  # noqa: F401
+from ._abi import (CM_EMAX, CM_KEY_NONE, CM_LAYOUT_BLK, CM_LAYOUT_DENSE, CM_LAYOUT_TRI4,  # noqa: F401
+                   CM_ROUND_RANDOMIZED,
                    CM_ROUND_THRESHOLD,
                    CM_NMAX)
 
@@ -32,9 +33,16 @@ def _check(status: int, where: str):
         raise CMError(status, where)
 
 
+LAYOUTS = {"dense": CM_LAYOUT_DENSE, "tri4": CM_LAYOUT_TRI4, "blk": CM_LAYOUT_BLK}
+
+
+def sstar_floats(n: int, layout: str, ld: int = 0) -> int:
+    """cm_sstar_floats: floats one S* occupies in a layout (the minimum stride)."""
+    return int(_lib.cm_sstar_floats(int(n), LAYOUTS[layout], int(ld)))
+
+
 def tri4_size(n: int) -> int:
-    q, m = divmod(n, 4)
-    return 8 * q * (q - 1) + 12 * q + (4 * q if m > 0 else 0) + max(m - 1, 0) * (4 * q + 4)
+    return sstar_floats(n, "tri4")
 
 
 class Graph:
@@ -214,8 +222,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
                        best_batch_key=None, init_keys: bool = False, overlap: bool = False):
     """cm_round_and_evaluate on device tensors.
 
-    sstar : float32 CUDA tensor; dense [N_S, n, ld] or tri4 [N_S, tri4_size(n)] (or any
-            buffer with explicit n_sstar / ld / stride).
+    sstar : float32 CUDA tensor; dense [N_S, n, ld], tri4 [N_S, tri4_size(n)] or blk
+            [N_S, sstar_floats(n, "blk")] (or any buffer with explicit n_sstar / ld / stride).
     theta : float32 CUDA tensor [N_theta] (deterministic rounding, Alg. 2 line 1), or None with
             ``samples`` = N samples per S* of randomized rounding (R1,
             Philox key ``seed``).
@@ -231,7 +239,7 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     """
     import torch
     n = graph.n
-    lay = {"dense": CM_LAYOUT_DENSE, "tri4": CM_LAYOUT_TRI4}[layout]
+    lay = LAYOUTS[layout]
     if n_sstar is None:
         n_sstar = sstar.shape[0]
     if lay == CM_LAYOUT_DENSE:
@@ -242,7 +250,7 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     else:
         ld = 0
         if stride is None:
-            stride = sstar.stride(0) if sstar.dim() == 2 else tri4_size(n)
+            stride = sstar.stride(0) if sstar.dim() == 2 else sstar_floats(n, layout)
     dev = sstar.device
     randomized = samples is not None
     if randomized == (theta is not None):

@@ -17,6 +17,7 @@ CM_NMAX = 1024
 CM_EMAX = 8192
 CM_LAYOUT_DENSE = 0
 CM_LAYOUT_TRI4 = 1
+CM_LAYOUT_BLK = 2
 CM_KEY_NONE = (1 << 63) - 1
 CM_ROUND_THRESHOLD = 0
 CM_ROUND_RANDOMIZED = 1
@@ -24,7 +25,7 @@ CM_EVAL_INIT_KEYS = 1
 CM_EVAL_OVERLAP = 2
 
 EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_bound",
-           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_debug_cta_trace_at",
+           "cm_round_and_evaluate", "cm_workspace_bytes", "cm_sstar_floats", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_debug_cta_trace_at",
            "cm_last_call_seq", "cm_stream_wait_call", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
            "cm_policy_checkpoints", "cm_policy_sstar", "cm_policy_last_error",
            "cm_last_error")
@@ -74,6 +75,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_graph_cost_bound.restype = ctypes.c_int64
     lib.cm_round_and_evaluate.argtypes = [P, ctypes.POINTER(EvalArgs), P]
     lib.cm_round_and_evaluate.restype = ctypes.c_int
+    lib.cm_sstar_floats.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
+    lib.cm_sstar_floats.restype = ctypes.c_int64
     lib.cm_workspace_bytes.argtypes = [P, ctypes.c_int64]
     lib.cm_workspace_bytes.restype = ctypes.c_int64
     lib.cm_debug_trace.argtypes = [P, ctypes.c_int32]

@@ -229,15 +229,12 @@ CUtensorMapL2promotion promo_of(int v) {
   }
 }
 CUtensorMapL2promotion l2_promotion() { return promo_of(env_flag("CM_L2PROMO", 256)); }
-// the block just before an odd diagonal block: a 256-byte window would also pull the diagonal
-// block's rows, upper-triangle bytes included (CM_L2PROMO_PRE, default 128)
-CUtensorMapL2promotion l2_promotion_pre() { return promo_of(env_flag("CM_L2PROMO_PRE", 128)); }
 
-const void* round_fn(int nt, bool bulk, bool rnd) {
-#define CM_R(NT) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, true, true>) \
-                              : reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, false, true>)) \
-                      : (bulk ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, true, false>) \
-                              : reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, false, false>)))
+// lay: 0 dense (tensor-map TMA), 1 tri4 (gather4 / per-row bulk copies), 2 blocked (one bulk copy per block)
+const void* round_fn(int nt, int lay, bool rnd) {
+#define CM_R1(NT, L) (rnd ? reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, L, true>) \
+                          : reinterpret_cast<const void*>(cm2::round_tma_kernel<NT, L, false>))
+#define CM_R(NT) (lay == 1 ? CM_R1(NT, 1) : lay == 2 ? CM_R1(NT, 2) : CM_R1(NT, 0))
   switch (nt) {
     case 1: return CM_R(1);
     case 2: return CM_R(2);
@@ -245,12 +242,12 @@ const void* round_fn(int nt, bool bulk, bool rnd) {
     default: return CM_R(4);
   }
 #undef CM_R
+#undef CM_R1
 }
-const void* fused_fn(int nt, bool bulk, bool rnd, bool s32) {
-#define CM_F(NT, ET) (rnd ? (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, true, int32_t>) \
-                                  : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, true, int32_t>)) \
-                          : (bulk ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, true, false, ET>) \
-                                  : reinterpret_cast<const void*>(cm2::fused_kernel<NT, false, false, ET>)))
+const void* fused_fn(int nt, int lay, bool rnd, bool s32) {
+#define CM_F1(NT, L, ET) (rnd ? reinterpret_cast<const void*>(cm2::fused_kernel<NT, L, true, int32_t>) \
+                              : reinterpret_cast<const void*>(cm2::fused_kernel<NT, L, false, ET>))
+#define CM_F(NT, ET) (lay == 1 ? CM_F1(NT, 1, ET) : lay == 2 ? CM_F1(NT, 2, ET) : CM_F1(NT, 0, ET))
   if (s32) {
     switch (nt) {
       case 1: return CM_F(1, int32_t);
@@ -266,6 +263,7 @@ const void* fused_fn(int nt, bool bulk, bool rnd, bool s32) {
     default: return CM_F(4, int64_t);
   }
 #undef CM_F
+#undef CM_F1
 }
 
 __global__ void init_keys_kernel(int64_t* best_key, int64_t* best_batch_key, int n_budget) {
@@ -326,16 +324,17 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   }
   int occ1 = 0, occ2 = 0;
   const int nib_staged = g->d_nib32 ? g->nib_entries : 0;
-  const bool bulk = a->layout == CM_LAYOUT_TRI4;                    // K1 by 1-D bulk copies (tri4) or tensor-map TMA
+  const bool bulk = a->layout == CM_LAYOUT_TRI4;                    // K1 stage form: tri4's 5 KB stages
+  const int lay = a->layout;                                        // K1 load path (round_fn / fused_fn)
   auto smem1_for = [&](int nt) { return cm2::k1_smem_bytes(nt, nib_staged, bulk); };
   {
     // scan_kernel wants the maximum shared-memory carve-out (its A' arrays are ~210 KB per SM).
     std::lock_guard<std::mutex> lock(attr_mu);
     if (!da.carve) {
       for (int nt = 1; nt <= 4; ++nt)
-        for (int bl = 0; bl < 2; ++bl)
+        for (int lay = 0; lay < 3; ++lay)
           for (int rd = 0; rd < 2; ++rd) {
-            const void* fn = round_fn(nt, bl != 0, rd != 0);
+            const void* fn = round_fn(nt, lay, rd != 0);
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max(cm2::k1_smem_bytes(1, 128 * 32, true), cm2::k1_smem_bytes(4, 128 * 32, true)));
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(round_tma_kernel)");
@@ -364,22 +363,13 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     const cuuint64_t dims[3] = {(cuuint64_t)a->ld, (cuuint64_t)n, (cuuint64_t)a->n_sstar};
     const cuuint64_t strides[2] = {(cuuint64_t)a->ld * 4, (cuuint64_t)a->sstar_stride * 4};
     const cuuint32_t box[3] = {32, 32, 1};
-    const cuuint32_t box8[3] = {8, 8, 1};
-    const cuuint32_t box16[3] = {16, 8, 1};
-    const cuuint32_t box32[3] = {32, 16, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    auto mk = [&](CUtensorMap* m, const cuuint32_t* bx, CUtensorMapSwizzle sw, CUtensorMapL2promotion pr) {
-      return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides, bx, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    auto mk = [&](CUtensorMap* m, CUtensorMapL2promotion pr) {
+      return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a->sstar), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     };
-    // off-diagonal blocks: 256-byte promotion (CM_L2PROMO); the block before an odd diagonal
-    // without it (cm2::DiagMaps); the diagonal's three boxes without any
-    const CUtensorMapL2promotion none = CU_TENSOR_MAP_L2_PROMOTION_NONE;
-    if (mk(&tmap, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion()) != CUDA_SUCCESS ||
-        mk(&dmaps.pre, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion_pre()) != CUDA_SUCCESS ||
-        mk(&dmaps.d8, box8, CU_TENSOR_MAP_SWIZZLE_32B, none) != CUDA_SUCCESS ||
-        mk(&dmaps.d16, box16, CU_TENSOR_MAP_SWIZZLE_64B, none) != CUDA_SUCCESS ||
-        mk(&dmaps.d32, box32, CU_TENSOR_MAP_SWIZZLE_128B, none) != CUDA_SUCCESS)
+    // off-diagonal blocks: 256-byte promotion (CM_L2PROMO); diagonal blocks: none (the rows end there)
+    if (mk(&tmap, l2_promotion()) != CUDA_SUCCESS || mk(&dmaps.diag, CU_TENSOR_MAP_L2_PROMOTION_NONE) != CUDA_SUCCESS)
       return fail(CM_EINVAL, "cuTensorMapEncodeTiled failed (alignment / sizes)");
   }
   // tri4: a 2-D map whose rows are the batch's 16-byte units (stride 16 B: overlapping 128-byte
@@ -401,7 +391,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     }
   }
   const bool rnd = a->rounding == CM_ROUND_RANDOMIZED;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, round_fn(4, bulk, rnd), 256, smem1_for(4));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, round_fn(4, lay, rnd), 256, smem1_for(4));
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, scan_fn, 32 * wpc, smem2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ1 < 1 || occ2 < 1) return fail(CM_ERANGE, "kernel does not fit on an SM");
@@ -493,7 +483,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
                                               (int64_t)G * ((((int64_t)a->n_sstar - 32 * (units - 1)) * nt + 31) / 32);
     if (smemf <= (size_t)g->smem_optin && R >= 1 && ctl_bytes(R) + R * slot_bytes <= set_bytes &&
         total_tasks < (int64_t(1) << 31)) {
-      const void* fn = fused_fn(nt, bulk, rnd, g->scan32);
+      const void* fn = fused_fn(nt, lay, rnd, g->scan32);
       {
         std::lock_guard<std::mutex> lock(attr_mu);
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemf);
@@ -640,7 +630,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       const int thr1 = 32 * wpb;
       const size_t sm1 = smem1_for(rp.nt);
       void* k1args[] = {&rp, &tmap, &dmaps};
-      e = cudaLaunchKernel(round_fn(rp.nt, bulk, rnd), dim3((unsigned)grid1), dim3((unsigned)thr1), k1args, sm1, g->st_round);
+      e = cudaLaunchKernel(round_fn(rp.nt, lay, rnd), dim3((unsigned)grid1), dim3((unsigned)thr1), k1args, sm1, g->st_round);
       if (e != cudaSuccess) break;
     }
     if (e != cudaSuccess) break;
@@ -1036,6 +1026,19 @@ int64_t cm_workspace_bytes(const cm_graph* g, int64_t chunk_candidates) {
   return 2 * cand_bytes(g->n, g->scan32) * ((chunk_candidates + 31) & ~int64_t(31));   // two buffers
 }
 
+int64_t cm_sstar_floats(int32_t n, int32_t layout, int64_t ld) {
+  if (n < 1) return -1;
+  switch (layout) {
+    case CM_LAYOUT_DENSE: return ld >= n ? (int64_t)n * ld : -1;
+    case CM_LAYOUT_TRI4: {
+      const int64_t q = n >> 2, m = n & 3;
+      return 8 * q * (q - 1) + 12 * q + (m > 0 ? 4 * q : 0) + (m > 1 ? (m - 1) * (4 * q + 4) : 0);
+    }
+    case CM_LAYOUT_BLK: return cm2::blk_size(n);
+  }
+  return -1;
+}
+
 int32_t cm_graph_n(const cm_graph* g) { return g ? g->n : -1; }
 int64_t cm_graph_cost_bound(const cm_graph* g) { return g ? g->cost_bound : -1; }
 
@@ -1043,18 +1046,14 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
   if (!g || !a) return fail(CM_EINVAL, "NULL graph or args");
   const int n = g->n;
   if (a->n_sstar < 0 || a->n_theta < 1 || a->n_budget < 0) return fail(CM_EINVAL, "bad counts");
-  if (a->layout != CM_LAYOUT_DENSE && a->layout != CM_LAYOUT_TRI4) return fail(CM_EINVAL, "bad layout");
+  if (a->layout != CM_LAYOUT_DENSE && a->layout != CM_LAYOUT_TRI4 && a->layout != CM_LAYOUT_BLK)
+    return fail(CM_EINVAL, "bad layout");
   if (a->rounding != CM_ROUND_THRESHOLD && a->rounding != CM_ROUND_RANDOMIZED) return fail(CM_EINVAL, "bad rounding");
   if (a->rounding == CM_ROUND_RANDOMIZED && a->index_base % a->n_theta != 0)
     return fail(CM_EINVAL, "randomized rounding: index_base must be a multiple of n_theta (samples)");
-  int64_t min_stride;
-  if (a->layout == CM_LAYOUT_DENSE) {
-    if (a->ld < n || (a->ld & 3)) return fail(CM_EINVAL, "ld must be >= n and a multiple of 4");
-    min_stride = (int64_t)n * a->ld;
-  } else {
-    const int64_t q = n >> 2, m = n & 3;
-    min_stride = 8 * q * (q - 1) + 12 * q + (m > 0 ? 4 * q : 0) + (m > 1 ? (m - 1) * (4 * q + 4) : 0);
-  }
+  if (a->layout == CM_LAYOUT_DENSE && (a->ld < n || (a->ld & 3)))
+    return fail(CM_EINVAL, "ld must be >= n and a multiple of 4");
+  const int64_t min_stride = cm_sstar_floats(n, a->layout, a->ld);
   if (a->n_sstar > 0) {
     if (a->sstar_stride < min_stride || (a->sstar_stride & 3))
       return fail(CM_EINVAL, "sstar_stride too small or not a multiple of 4");
@@ -1098,8 +1097,9 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);
   }
-  if (a->rounding != CM_ROUND_THRESHOLD || a->best_batch_key)
-    return fail(CM_ERANGE, "randomized rounding / max-batch need the stage-sliced kernels (graph too large for them)");
+  if (a->rounding != CM_ROUND_THRESHOLD || a->best_batch_key || a->layout == CM_LAYOUT_BLK)
+    return fail(CM_ERANGE, "randomized rounding / max-batch / the blocked layout need the stage-sliced kernels "
+                           "(graph too large for them)");
 
   const int G = (n + 31) / 32;
   const int tri_words = 16 * G * (G + 1);

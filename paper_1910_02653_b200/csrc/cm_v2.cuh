@@ -69,6 +69,27 @@ __device__ __forceinline__ int64_t row_offset(int layout, int64_t ld, int r) {
   return 8 * q * (q - 1) + 12 * q + (m > 0 ? 4 * q : 0) + (m > 1 ? (m - 1) * (4 * q + 4) : 0);
 }
 
+// CM_LAYOUT_BLK, the blocked strict lower triangle (include/cm.h): row group g = rows
+// 32g+1 .. 32g+h_g (h_g = min(32, n-1-32g)), blocks w = 0..g of 32 nodes, stored group after
+// group, block after block; an off-diagonal block is h_g rows x 32 floats with 16-byte chunk c
+// of row l at chunk c ^ (l & 7) (the 128-byte swizzle of the K1 tile), the diagonal block
+// chunk-major: chunk c of rows l = 4c .. h_g-1.  Every group but the last is full (h = 32):
+// 128 g (g-1) + 144 g chunks precede group g.
+__host__ __device__ __forceinline__ int blk_rows(int n, int g) { return min(32, n - 1 - 32 * g); }
+__host__ __device__ __forceinline__ int blk_diag_chunks(int h) {
+  int c = 0;
+  for (int k = 0; k < 8; ++k) c += max(0, h - 4 * k);
+  return c;
+}
+__host__ __device__ __forceinline__ int64_t blk_block_off(int g, int w, int h) {   // floats
+  return 4 * (128 * (int64_t)g * (g - 1) + 144 * (int64_t)g) + (int64_t)32 * h * w;
+}
+__host__ __device__ __forceinline__ int64_t blk_size(int n) {                      // floats per S*
+  if (n < 2) return 0;
+  const int Gr = (n - 2) / 32 + 1, h = blk_rows(n, Gr - 1);
+  return blk_block_off(Gr - 1, Gr - 1, h) + 4 * (int64_t)blk_diag_chunks(h);
+}
+
 // 32x32 bit transpose across a warp: in, lane l holds row word l (bit c = A[l][c]);
 // out, lane l holds column word l (bit r = A[r][l]).
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
@@ -302,9 +323,10 @@ struct K1Plain {
 };
 
 // Per-CTA K1 set-up (staged mass table, mbarriers); the caller synchronises the CTA after it.
-template <int NT, bool BULK, bool RAND>
+template <int NT, int LAY, bool RAND>
 __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1smem, int nwarps1, int tid,
                                          int nthreads) {
+  constexpr bool BULK = LAY == 1;
   constexpr int kSt = k1_stages(NT);
   int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT, BULK));
   if (p.nib32)
@@ -314,27 +336,14 @@ __device__ __forceinline__ void k1_setup(const RoundParams& p, unsigned char* k1
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Dense diagonal blocks (w = g): row 32g+1+l holds only nodes 32g .. 32g+l of the block, so
-// the block is read as three boxes that stop where the rows' stored prefixes stop (Eq. 12b,
-// entries i >= t are never read): rows l = 0..7 x 8 nodes (32-byte rows,
-// SWIZZLE_32B) at stage byte 0, rows 8..15 x 16 nodes (64-byte rows, SWIZZLE_64B) at 512,
-// rows 16..31 x 32 nodes (SWIZZLE_128B, exactly the full tile's rows 16..31) at 2048:
-// 2 816 of the full tile's 4 096 bytes, none of them promoted past the block.  Each box's
-// swizzle keeps its 8 lanes' 16-byte reads on 8 distinct bank groups.  `pre`: the full box
-// without 256-byte L2 promotion, for block w = g-1 when w is even (its promotion window
-// would otherwise pull the diagonal block's whole 128-byte rows from DRAM).
+// Dense diagonal blocks (w = g): the full {32, 32} box through a map without L2 promotion (the
+// rows end inside the block).  Measured: reading only the rows' stored prefixes (boxes of 8x8,
+// 16x8 and 32x16 nodes x rows, 2 816 instead of 4 096 bytes) cut the L2 -> SM bytes by 14 KB
+// per S* but not one DRAM byte -- a missed 32-byte sector brings its whole 128-byte line from
+// DRAM -- and cost 4 % more instructions; the blocked layout (CM_LAYOUT_BLK) removes the bytes.
 struct DiagMaps {
-  CUtensorMap pre;     // box {32 nodes, 32 rows}, SWIZZLE_128B, 128-byte promotion
-  CUtensorMap d8;      // box {8, 8}, SWIZZLE_32B, no promotion
-  CUtensorMap d16;     // box {16, 8}, SWIZZLE_64B, no promotion
-  CUtensorMap d32;     // box {32, 16}, SWIZZLE_128B, no promotion
+  CUtensorMap diag;    // box {32 nodes, 32 rows}, SWIZZLE_128B, no promotion
 };
-constexpr uint32_t kDiagBytes = 8 * 32 + 8 * 64 + 16 * 128;
-// lane l's row in a diagonal stage: byte offset of the row and the XOR of its 16-byte chunks
-__device__ __forceinline__ uint32_t diag_row_off(int l) { return l < 8 ? 32u * l : l < 16 ? 512u + 64u * (l - 8) : 128u * l; }
-__device__ __forceinline__ uint32_t diag_row_xor(int l) {
-  return l < 8 ? (uint32_t)((l >> 2) & 1) << 4 : l < 16 ? (uint32_t)(((l - 8) >> 1) & 3) << 4 : (uint32_t)(l & 7) << 4;
-}
 
 // K1 body of one warp: S* s = hk.first(), hk.next(s), ... while < s_count; wl = the warp's
 // index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
@@ -342,10 +351,12 @@ __device__ __forceinline__ uint32_t diag_row_xor(int l) {
 // takes queue in `sq` (8 per warp) until the consumer reaches them.
 // RAND: randomized rounding, sample th0 + j instead of threshold th0 + j (one Philox block
 // per four consecutive nodes and sample).
-template <int NT, bool BULK, bool RAND, class Hooks>
+template <int NT, int LAY, bool RAND, class Hooks>
 __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const DiagMaps* dmaps,
                                         unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
+  constexpr bool BULK = LAY == 1;                                   // tri4
+  constexpr bool BLK = LAY == 2;                                    // blocked triangle (CM_LAYOUT_BLK)
   constexpr int kSt = k1_stages(NT);
   constexpr uint32_t kStageBytes = (uint32_t)k1_stage_bytes(BULK);
   int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT, BULK));   // p.nib32 staged (if any)
@@ -364,7 +375,6 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
 #pragma unroll
   for (int j = 0; j < NT; ++j) th[j] = RAND ? 0.f : p.theta[p.th0 + j];
   const Transposer transpose(lane);
-  const uint32_t drow_off = diag_row_off(lane), drow_xor = diag_row_xor(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t tiles_u32 = smem_u32(tiles);
   // tri4 read by gather4 lands in the same 128-byte-swizzled form as the dense tensor tiles.
@@ -372,7 +382,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   // 128-byte window may run past the buffer -- so those take per-row bulk copies of exactly the
   // stored floats into the 144-byte-pitch form.
   auto pitched_of = [&](int s_rel) { return BULK && (!p.g4 || p.s_begin + s_rel >= p.g4_end); };
-  const uint64_t pol = (!BULK && p.evict_first) ? l2_evict_first_policy() : 0ull;
+  const uint64_t pol = (LAY == 0 && p.evict_first) ? l2_evict_first_policy() : 0ull;
 
   // Producer cursor (ps, pg, pw) runs kSt-1 blocks ahead of the consumer.  No proxy
   // fence before re-filling a stage: its previous contents were consumed (ballots issued on
@@ -409,6 +419,16 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)lane * kBulkPitch, src, 4u * (uint32_t)len,
                   &bars[pstage]);
       }
+    } else if (BLK) {
+      // blocked triangle: block (pg, pw) is one contiguous run of the S* -- one 1-D bulk copy
+      // (UBLKCP) of exactly its stored bytes, already in the stage's read form
+      if (lane == 0) {
+        const int h = blk_rows(p.n, pg);
+        const uint32_t bytes = pw < pg ? 128u * (uint32_t)h : 16u * (uint32_t)blk_diag_chunks(h);
+        mbar_expect_tx(&bars[pstage], bytes);
+        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes,
+                  p.sstar + (p.s_begin + ps) * p.stride + blk_block_off(pg, pw, h), bytes, &bars[pstage]);
+      }
     } else if (lane == 0) {
 #ifdef CM_EXP_L2INPUT
       const int z = (int)((p.s_begin + ps) & 63);                   // timing experiment
@@ -416,17 +436,10 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
       const int z = (int)(p.s_begin + ps);
 #endif
       unsigned char* dst = tiles + (size_t)pstage * kStageBytes;
-      if (pw == pg) {                                               // diagonal: the rows' prefixes only
-        mbar_expect_tx(&bars[pstage], kDiagBytes);
-        tma_load_3d(dst, &dmaps->d8, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
-        tma_load_3d(dst + 512, &dmaps->d16, 32 * pw, 32 * pg + 9, z, &bars[pstage]);
-        tma_load_3d(dst + 2048, &dmaps->d32, 32 * pw, 32 * pg + 17, z, &bars[pstage]);
-      } else {
-        mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
-        const CUtensorMap* tm = (pw + 1 == pg && (pw & 1) == 0) ? &dmaps->pre : tmap;
-        if (pol) tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage], pol);
-        else tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
-      }
+      mbar_expect_tx(&bars[pstage], 32u * 32u * 4u);
+      const CUtensorMap* tm = pw == pg ? &dmaps->diag : tmap;
+      if (pol) tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage], pol);
+      else tma_load_3d(dst, tm, 32 * pw, 32 * pg + 1, z, &bars[pstage]);
     }
     pstage = pstage + 1 == kSt ? 0 : pstage + 1;
     if (++pw > pg) {
@@ -451,7 +464,17 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     uint32_t* out = hk.begin(s);
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
-      // rows of the group that exist (r < n): bits [0, hi)
+      // BLK diagonal block: chunk c of this lane's row at byte 16 lane + dgo[c] of the stage
+      uint32_t dgo[8];
+      if (BLK) {
+        const int h = blk_rows(p.n, g);
+        int b = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          dgo[c] = 16u * (uint32_t)(b - 4 * c);
+          b += max(0, h - 4 * c);
+        }
+      }
       int64_t mass[NT];
 #pragma unroll
       for (int j = 0; j < NT; ++j) mass[j] = 0;
@@ -459,19 +482,23 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         issue();
         mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
         phase_bits ^= 1u << cstage;
-        // this lane's row in the stage: the 144-byte-pitch per-row form (tri4 fallback), the
-        // three diagonal boxes (dense, w = g) or the 128-byte-swizzled 32 x 32 tile
+        // this lane's row in the stage: the 144-byte-pitch per-row form (tri4 fallback) or the
+        // 128-byte-swizzled 32 x 32 tile
+        // (BLK: off-diagonal blocks are stored in the tile's swizzled form; the diagonal block
+        // chunk-major, so a quarter-warp's 16-byte reads of one chunk are consecutive)
         const bool pitched = pitched_of(s);
-        const bool dg = !BULK && w == g;
+        const bool bdiag = BLK && w == g;
         const uint32_t rb = tiles_u32 + (uint32_t)cstage * kStageBytes +
-                            (pitched ? (uint32_t)lane * (uint32_t)kBulkPitch : dg ? drow_off : 128u * (uint32_t)lane);
-        const uint32_t sw = pitched ? 0u : dg ? drow_xor : (uint32_t)(lane & 7) << 4;
+                            (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : bdiag ? 16u : 128u);
+        const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
         float x[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float4 v;
+          // (rows l < 4c have no chunk c: any in-stage address will do, the bits are masked)
+          const uint32_t off = bdiag ? (lane >= 4 * c ? dgo[c] : 0u) : (((uint32_t)c << 4) ^ sw);
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + (((uint32_t)c << 4) ^ sw)));
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + off));
           x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
         }
         cstage = cstage + 1 == kSt ? 0 : cstage + 1;
@@ -569,17 +596,17 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   }
 }
 
-template <int NT, bool BULK, bool RAND>
+template <int NT, int LAY, bool RAND>
 __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const RoundParams p, const __grid_constant__ CUtensorMap tmap,
                                                                     const __grid_constant__ DiagMaps dmaps) {
   extern __shared__ __align__(1024) unsigned char k1raw[];
   unsigned char* k1smem = k1raw + ((1024u - (smem_u32(k1raw) & 1023u)) & 1023u);
-  k1_setup<NT, BULK, RAND>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
+  k1_setup<NT, LAY, RAND>(p, k1smem, (int)(blockDim.x >> 5), (int)threadIdx.x, (int)blockDim.x);
   __syncthreads();
   __shared__ int sq[32][8];
   const K1Plain hk{p.sn, p.n_theta, p.th0, p.cs, (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
                    (int)((gridDim.x * blockDim.x) >> 5)};
-  k1_body<NT, BULK, RAND>(p, &tmap, &dmaps, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
+  k1_body<NT, LAY, RAND>(p, &tmap, &dmaps, k1smem, (int)(threadIdx.x >> 5), sq[threadIdx.x >> 5], hk);
 }
 
 
@@ -1323,7 +1350,7 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
 }
 
 // ET: the scan state (int32 when sum M / gcd < 2^31, else int64).
-template <int NT, bool BULK, bool RAND, typename ET>
+template <int NT, int LAY, bool RAND, typename ET>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const __grid_constant__ DiagMaps dmaps) {
@@ -1339,7 +1366,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   extern __shared__ __align__(1024) unsigned char fraw[];
   unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
   unsigned char* k1smem = base;
-  unsigned char* k2smem = base + fused_k1_bytes(NT, fp.rp.nib32 ? fp.rp.nib_entries : 0, BULK);
+  unsigned char* k2smem = base + fused_k1_bytes(NT, fp.rp.nib32 ? fp.rp.nib_entries : 0, LAY == 1);
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& sp = fp.sp;
@@ -1352,7 +1379,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     __threadfence();
     atomicExch(fp.ctl + 3 + 3 * (int64_t)fp.n_slots, 2u);
   }
-  k1_setup<NT, BULK, RAND>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
+  k1_setup<NT, LAY, RAND>(fp.rp, k1smem, KF1, (int)threadIdx.x, (int)blockDim.x);
   for (int i = threadIdx.x; i < sp.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(k2smem)[i] = sp.blob[i];
   if (warp == kFirstScanWarp) {
@@ -1369,7 +1396,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     __shared__ int sq[KF1][8];
     const int w1 = kK1High ? warp - kFusedScanWarps : warp;
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
-    k1_body<NT, BULK, RAND>(fp.rp, &tmap, &dmaps, k1smem, w1, sq[w1], hk);
+    k1_body<NT, LAY, RAND>(fp.rp, &tmap, &dmaps, k1smem, w1, sq[w1], hk);
     if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 1), globaltimer());
     fused_exit(fp);
     return;

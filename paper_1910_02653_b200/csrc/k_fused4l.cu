@@ -1,3 +1,3 @@
 // Instances: fused persistent kernels, int64 scan state, 4 threshold(s) per pass (see cm_inst.cuh).
 #include "cm_inst.cuh"
-CM_FUSED(4, false, false, int64_t) CM_FUSED(4, true, false, int64_t)
+CM_FUSED(4, 0, false, int64_t) CM_FUSED(4, 1, false, int64_t) CM_FUSED(4, 2, false, int64_t)

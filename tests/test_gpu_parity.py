@@ -6,13 +6,14 @@ import pytest
 from oracle import Instance, best_per_budget, evaluate, masks_u64
 from workloads import budgets as B
 from workloads import graphs as G
-from workloads.sstar import dense_to_tri4, from_binary, gen_sstar, roundup4
+from workloads.sstar import dense_to_blk, dense_to_tri4, from_binary, gen_sstar, roundup4
 
 pytestmark = pytest.mark.gpu
 
 KEY_NONE = (1 << 63) - 1
-# dense: K1 reads 32x32 blocks by tensor-map TMA; tri4: by per-row 1-D bulk copies
-LAYOUTS = ["dense", "tri4"]
+# dense: K1 reads 32x32 blocks by tensor-map TMA; tri4: by tile::gather4 (per-row 1-D bulk copies
+# for a batch's last S*); blk (CM_LAYOUT_BLK): one 1-D bulk copy per block
+LAYOUTS = ["dense", "tri4", "blk"]
 
 
 def gpu_run(g, sstar, thetas, budgets=None, layout="dense", masks=False, index_base=0,
@@ -43,7 +44,7 @@ def oracle_run(g, sstar_dense, thetas, keep=False):
 
 def compare(g, sstar_dense, thetas, budgets=None, masks=False, layout="dense", index_base=0,
             total=None):
-    src = sstar_dense if layout == "dense" else dense_to_tri4(sstar_dense)
+    src = {"dense": lambda x: x, "tri4": dense_to_tri4, "blk": lambda x: dense_to_blk(x, upper=np.nan)}[layout](sstar_dense)
     res = gpu_run(g, src, thetas, budgets, layout=layout, masks=masks, index_base=index_base,
                   total=total, ld=sstar_dense.shape[2] if layout == "dense" else None)
     inst, outs = oracle_run(g, sstar_dense, thetas, keep=masks)
@@ -196,7 +197,8 @@ def test_max_n(layout):
 def test_device_generator_matches_host():
     import torch
     from workloads.device_gen import DeviceGenerator
-    for name, fam, layout in [("resnet50", "mix", "dense"), ("unet", "g1", "tri4"), ("vgg16", "g2", "dense")]:
+    for name, fam, layout in [("resnet50", "mix", "dense"), ("unet", "g1", "tri4"), ("vgg16", "g2", "dense"),
+                              ("resnet50", "g1", "blk"), ("fcn8", "mix", "blk")]:
         g = G.NETWORKS[name]()
         dg = DeviceGenerator(g, fam, 1234, layout=layout)
         buf = torch.empty(dg.shape(6), dtype=torch.float32, device="cuda")

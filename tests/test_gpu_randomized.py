@@ -7,7 +7,7 @@ from oracle import Instance, best_per_budget, evaluate, evaluate_randomized, mas
 from oracle.randomized import round_S_randomized
 from workloads import budgets as B
 from workloads import graphs as G
-from workloads.sstar import dense_to_tri4, from_binary, gen_sstar
+from workloads.sstar import dense_to_blk, dense_to_tri4, from_binary, gen_sstar
 
 pytestmark = pytest.mark.gpu
 KEY_NONE = (1 << 63) - 1
@@ -18,7 +18,7 @@ def run_rand(g, x_dense, samples, seed, budgets=None, layout="dense", masks=Fals
     import paper_1910_02653_b200 as cm
     dev = torch.device("cuda:0")
     graph = cm.Graph.from_workload(g)
-    src = x_dense if layout == "dense" else dense_to_tri4(x_dense)
+    src = {"dense": lambda x: x, "tri4": dense_to_tri4, "blk": dense_to_blk}[layout](x_dense)
     x = torch.from_numpy(np.ascontiguousarray(src)).to(dev)
     bu = None if budgets is None else torch.tensor(np.asarray(budgets, np.int64), device=dev)
     out = cm.round_and_evaluate(graph, x, None, bu, layout=layout, masks=masks, samples=samples, seed=seed,
@@ -56,7 +56,7 @@ def check(g, x, samples, seed, budgets=None, layout="dense", masks=False, index_
     return res
 
 
-@pytest.mark.parametrize("layout", ["dense", "tri4"])
+@pytest.mark.parametrize("layout", ["dense", "tri4", "blk"])
 @pytest.mark.parametrize("samples", [1, 3, 4, 6])
 def test_small_randomized(layout, samples):
     """samples <= 4: the fused kernel (one Philox block per element gives four samples);

@@ -101,3 +101,53 @@ def test_budget_grid():
     grid = B.geometric_grid(g, 16)
     assert len(grid) == 16 and (np.diff(grid) > 0).all()
     assert grid[-1] == B.p_live(g) and grid[0] >= B.p_floor(g)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 32, 33, 34, 64, 65, 89, 213, 353, 401, 563, 1024])
+def test_blk_layout_is_a_bijection(n):
+    """CM_LAYOUT_BLK: every strict-lower entry (r, i) has its own float position inside the
+    S*'s blk_size(n) floats; the size agrees with the library's cm_sstar_floats."""
+    import ctypes
+    from paper_1910_02653_b200 import _abi
+    from workloads.sstar import blk_positions, blk_size
+    lib = _abi.load()
+    assert lib.cm_sstar_floats(n, 2, 0) == blk_size(n)
+    r, i, pos = blk_positions(n)
+    assert len(pos) == n * (n - 1) // 2
+    assert len(np.unique(pos)) == len(pos)
+    assert (pos >= 0).all() and (pos < max(1, blk_size(n))).all()
+    assert blk_size(n) % 4 == 0
+    del ctypes
+
+
+def test_blk_layout_small_case_by_hand():
+    """n = 6 (one group of h = 5 rows, one diagonal block, chunk-major): chunk 0 of rows
+    l = 0..4 at chunks 0..4, chunk 1 (nodes 4..7) of row l = 4 (r = 5) at chunk 5."""
+    from workloads.sstar import blk_positions, blk_size, dense_to_blk
+    assert blk_size(6) == 4 * (5 + 1)
+    x = np.zeros((1, 6, 8), np.float32)
+    for r in range(6):
+        for i in range(r):
+            x[0, r, i] = 10 * r + i
+    b = dense_to_blk(x, upper=-1.0)[0]
+    assert list(b[0:4]) == [10, -1, -1, -1]                   # row 1: node 0
+    assert list(b[16:20]) == [50, 51, 52, 53]                 # row 5 (l = 4), chunk 0
+    assert list(b[20:24]) == [54, -1, -1, -1]                 # row 5, chunk 1 (node 4)
+    r, i, pos = blk_positions(6)
+    assert dict(zip(zip(r.tolist(), i.tolist()), pos.tolist()))[(3, 2)] == 4 * 2 + 2
+
+
+def test_blk_layout_offdiagonal_swizzle():
+    """n = 40: group 1 holds rows 33..39 (h = 7); its block w = 0 is 7 rows x 32 floats with
+    chunk c of row l at chunk c ^ l; group 0's 32 x 32 diagonal block (576 floats) precedes it."""
+    from workloads.sstar import dense_to_blk
+    x = np.zeros((1, 40, 40), np.float32)
+    for r in range(40):
+        for i in range(r):
+            x[0, r, i] = 1000 * r + i
+    b = dense_to_blk(x)[0]
+    base = 576
+    for l in range(7):
+        for c in range(8):
+            assert list(b[base + 32 * l + 4 * (c ^ l): base + 32 * l + 4 * (c ^ l) + 4]) == \
+                [1000 * (33 + l) + 4 * c + e for e in range(4)]

@@ -1,0 +1,9 @@
+# round 2, GPU run B: blocked layout, re-read R1 randomized rounding
+set -x
+O=gpurun_out/r2b
+mkdir -p $O
+timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_randomized.py -q -x --timeout 600 > $O/tests.log 2>&1; echo "rc=$?" >> $O/tests.log
+for lay in blk dense; do timeout 300 python bench.py --layout $lay --steps 10 --no-cpu-baseline --no-e2e > $O/bench_resnet50_$lay.json 2> $O/bench_resnet50_$lay.err; done
+for c in vgg16 unet mobilenet fcn8; do timeout 300 python bench.py --config $c --layout blk --steps 10 --no-cpu-baseline --no-e2e > $O/bench_${c}_blk.json 2> $O/bench_${c}_blk.err; done
+for k in 1 2 4; do timeout 300 python bench.py --samples $k --layout blk --steps 5 --no-cpu-baseline --no-e2e > $O/bench_rand$k.json 2> $O/bench_rand$k.err; done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -s 3 -c 1 -o $O/fused_blk python bench.py --layout blk --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --overlap off > $O/ncu_full.log 2>&1

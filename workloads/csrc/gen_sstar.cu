@@ -23,6 +23,17 @@ __device__ __forceinline__ int64_t row_offset(int layout, int64_t ld, int r) {
   return 8 * q * (q - 1) + 12 * q + (m > 0 ? 4 * q : 0) + (m > 1 ? (m - 1) * (4 * q + 4) : 0);
 }
 
+// CM_LAYOUT_BLK (include/cm.h): float position of entry (r, i), i < r, within an S*
+__device__ __forceinline__ int64_t blk_pos(int n, int r, int i) {
+  const int g = (r - 1) >> 5, l = (r - 1) & 31, w = i >> 5, q = i & 31, c = q >> 2, e = q & 3;
+  const int h = min(32, n - 1 - 32 * g);
+  const int64_t base = 4 * (128 * (int64_t)g * (g - 1) + 144 * (int64_t)g) + (int64_t)32 * h * w;
+  if (w < g) return base + 32 * l + 4 * (c ^ (l & 7)) + e;
+  int b = 0;
+  for (int k = 0; k < c; ++k) b += max(0, h - 4 * k);
+  return base + 4 * (b + l - 4 * c) + e;
+}
+
 constexpr int PHI24 = 16777, PSI24 = 16777;
 __constant__ int RHO24[3] = {1677722, 5033165, 10066330};
 constexpr float INV24 = 1.0f / 16777216.0f;
@@ -56,9 +67,13 @@ __global__ void gen_kernel(int n, int L, const int32_t* __restrict__ last, const
     }
     __syncthreads();
   }
+  if (layout == 2) {                                  // blocked: fill, then place the entries
+    for (int64_t j = threadIdx.x; j < stride; j += blockDim.x) dst[j] = upper;
+    __syncthreads();
+  }
   for (int r = 0; r < n; ++r) {
-    float* row = dst + row_offset(layout, ld, r);
-    const int rowlen = layout == 0 ? (int)ld : ((r + 3) & ~3);
+    float* row = dst + (layout == 2 ? 0 : row_offset(layout, ld, r));
+    const int rowlen = layout == 0 ? (int)ld : layout == 1 ? ((r + 3) & ~3) : r;
     for (int i = threadIdx.x; i < rowlen; i += blockDim.x) {
       if (i >= r) { row[i] = upper; continue; }
       const uint64_t key = ((uint64_t)r << 32) | (uint64_t)i;
@@ -79,7 +94,8 @@ __global__ void gen_kernel(int n, int L, const int32_t* __restrict__ last, const
         if (q < PHI24) v = (float)(mix64(seed, 6, s, key) >> 40) * INV24;
         else if (q < PHI24 + PSI24) v = 0.5f;
       }
-      row[i] = v;
+      if (layout == 2) dst[blk_pos(n, r, i)] = v;
+      else row[i] = v;
     }
   }
 }

@@ -8,7 +8,7 @@ import os
 
 import numpy as np
 
-from .sstar import FAMILY_IDS, SIGMA_SCALE, roundup4, tri4_size
+from .sstar import FAMILY_IDS, SIGMA_SCALE, blk_size, roundup4, tri4_size
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcm_gen.so")
 _lib = None
@@ -41,9 +41,14 @@ class DeviceGenerator:
         if layout == "dense":
             self.ld = roundup4(n) if ld is None else int(ld)
             self.stride = n * self.ld
-        else:
+        elif layout == "tri4":
             self.ld = 0
             self.stride = tri4_size(n)
+        elif layout == "blk":
+            self.ld = 0
+            self.stride = blk_size(n)
+        else:
+            raise ValueError(layout)
         self.last = torch.tensor(graph.last_use().astype(np.int32), device=device)
         self.lastF = torch.tensor(graph.last_forward_use().astype(np.int32), device=device)
 
@@ -59,7 +64,7 @@ class DeviceGenerator:
             stream = torch.cuda.current_stream(out.device).cuda_stream
         rc = lib.cmgen_sstar(self.g.n, self.g.L, self.last.data_ptr(), self.lastF.data_ptr(),
                              self.family, self.seed, int(s_begin), int(count),
-                             0 if self.layout == "dense" else 1, self.ld, self.stride,
+                             {"dense": 0, "tri4": 1, "blk": 2}[self.layout], self.ld, self.stride,
                              float(upper), float(SIGMA_SCALE), out.data_ptr(), ctypes.c_void_p(stream))
         if rc != 0:
             raise RuntimeError(f"cmgen_sstar failed: cudaError {rc}")

@@ -146,13 +146,66 @@ def family_of(family: str, seed: int, s: int) -> str:
     return family
 
 
+def blk_rows(n: int, g: int) -> int:
+    return min(32, n - 1 - 32 * g)
+
+
+def blk_diag_chunks(h: int) -> int:
+    return sum(max(0, h - 4 * k) for k in range(8))
+
+
+def blk_block_off(g: int, w: int, h: int) -> int:
+    """Float offset of block (g, w) in a CM_LAYOUT_BLK S* (every group before g is full)."""
+    return 4 * (128 * g * (g - 1) + 144 * g) + 32 * h * w
+
+
+def blk_size(n: int) -> int:
+    """Floats per S* in CM_LAYOUT_BLK (include/cm.h)."""
+    if n < 2:
+        return 0
+    gr = (n - 2) // 32 + 1
+    h = blk_rows(n, gr - 1)
+    return blk_block_off(gr - 1, gr - 1, h) + 4 * blk_diag_chunks(h)
+
+
+def blk_positions(n: int):
+    """(rows, cols, positions): the float position of every strict-lower entry (r, i) in the
+    blocked layout: row group g = (r-1) div 32, row l = (r-1) mod 32 of it, block w = i div 32;
+    off-diagonal blocks row-major with 16-byte chunk c of row l at chunk c ^ (l mod 8), the
+    diagonal block chunk-major (chunk c of rows l = 4c .. h-1)."""
+    r, i = np.tril_indices(n, -1)
+    g, l = (r - 1) // 32, (r - 1) % 32
+    w, q = i // 32, i % 32
+    c, e = q // 4, q % 4
+    h = np.minimum(32, n - 1 - 32 * g)
+    base = 4 * (128 * g * (g - 1) + 144 * g) + 32 * h * w
+    off = base + 32 * l + 4 * (c ^ (l % 8)) + e
+    bc = np.zeros_like(c)
+    for k in range(8):
+        bc += np.where(k < c, np.maximum(0, h - 4 * k), 0)
+    diag = base + 4 * (bc + l - 4 * c) + e
+    return r, i, np.where(w < g, off, diag)
+
+
+def dense_to_blk(dense: np.ndarray, upper: float = 0.0) -> np.ndarray:
+    """Repack [count][n][ld] dense S* into CM_LAYOUT_BLK (strict lower part only)."""
+    count, n, _ = dense.shape
+    out = np.full((count, blk_size(n)), np.float32(upper), np.float32)
+    r, i, pos = blk_positions(n)
+    out[:, pos] = dense[:, r, i]
+    return out
+
+
 def gen_sstar(graph, family: str, seed: int, s_begin: int, count: int,
               layout: str = "dense", ld: int | None = None, upper: float = 0.0) -> np.ndarray:
     """Generate S* #s_begin .. s_begin+count-1 for ``graph``.
 
-    Returns float32 array [count][n][ld] (dense) or [count][tri4_size(n)] (tri4).
+    Returns float32 array [count][n][ld] (dense), [count][tri4_size(n)] (tri4) or
+    [count][blk_size(n)] (blk).
     """
     n = graph.n
+    if layout == "blk":
+        return dense_to_blk(gen_sstar(graph, family, seed, s_begin, count, upper=upper), upper=upper)
     if layout == "dense":
         ld = roundup4(n) if ld is None else ld
         assert ld >= n and ld % 4 == 0
