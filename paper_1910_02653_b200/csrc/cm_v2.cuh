@@ -176,6 +176,28 @@ __device__ __forceinline__ void pack_gt(uint32_t& w, const float* x, float th) {
   }
 }
 
+// The same 32 compares with packed fp32: d = theta - x by FADD2 (sub.rn.f32x2, no flush to zero)
+// for a pair of elements, and x > theta  <=>  sign(d) = 1: the rounded difference keeps the
+// exact difference's sign (denormals are kept), x = theta gives +0, NaN gives the canonical
+// NaN 0x7fffffff (sign 0), and theta is +0 rather than -0 (the caller adds 0.0f: -0 - (+0) =
+// -0 would set the bit for x = +0).  Each sign bit is funnel-shifted into the word (SHF): 1.5
+// instructions per element instead of 2.  Bit q of the word = element q; two chains (q >= 16,
+// q < 16) for ILP.  tt = theta in both halves.
+__device__ __forceinline__ uint32_t pack_sub(const uint64_t (&xp)[16], uint64_t tt) {
+  uint32_t hi = 0u, lo = 0u;
+#pragma unroll
+  for (int k = 15; k >= 8; --k) {
+    uint64_t d, e;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(tt), "l"(xp[k]));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e) : "l"(tt), "l"(xp[k - 8]));
+    hi = __funnelshift_l((uint32_t)(d >> 32), hi, 1);                // element 2k+1
+    hi = __funnelshift_l((uint32_t)d, hi, 1);                        // element 2k
+    lo = __funnelshift_l((uint32_t)(e >> 32), lo, 1);                // element 2k-15
+    lo = __funnelshift_l((uint32_t)e, lo, 1);                        // element 2k-16
+  }
+  return (hi << 16) | lo;
+}
+
 // Philox4x32-10 (Salmon et al., SC'11); the uniform is (word >> 8) * 2^-24, exact in fp32.
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -371,9 +393,12 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     for (int s = hk.first(); s < p.s_count; s = hk.next(s)) { hk.begin(s); hk.end(s); }
     return;
   }
-  float th[NT];
+  uint64_t tt[NT];                                                  // theta (-0 -> +0) in both halves
 #pragma unroll
-  for (int j = 0; j < NT; ++j) th[j] = RAND ? 0.f : p.theta[p.th0 + j];
+  for (int j = 0; j < NT; ++j) {
+    const uint32_t b = __float_as_uint(RAND ? 0.f : p.theta[p.th0 + j] + 0.0f);
+    tt[j] = ((uint64_t)b << 32) | b;
+  }
   const Transposer transpose(lane);
   const bool scaled32 = p.nib32 != nullptr;
   const uint32_t tiles_u32 = smem_u32(tiles);
@@ -391,6 +416,11 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   unsigned qhead = 0, qtail = 0;                                    // sq ring (warp-uniform)
   if (lane == 0) sq[0] = ps;
   ++qhead;
+  // BLK: the blocks are read in storage order, so the source is a running pointer; every group
+  // but the last (h_last rows) is full: 4 KB off-diagonal, 2 304-byte diagonal blocks
+  const int h_last = BLK ? blk_rows(p.n, Gr - 1) : 32;
+  const uint32_t diag_last = BLK ? 16u * (uint32_t)blk_diag_chunks(h_last) : 0u;
+  const float* psrc = BLK && ps < p.s_count ? p.sstar + (p.s_begin + ps) * p.stride : p.sstar;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
     if (BULK && !pitched_of(ps)) {
@@ -422,13 +452,13 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     } else if (BLK) {
       // blocked triangle: block (pg, pw) is one contiguous run of the S* -- one 1-D bulk copy
       // (UBLKCP) of exactly its stored bytes, already in the stage's read form
+      const bool last = pg == Gr - 1;
+      const uint32_t bytes = pw < pg ? (last ? 128u * (uint32_t)h_last : 4096u) : (last ? diag_last : 2304u);
       if (lane == 0) {
-        const int h = blk_rows(p.n, pg);
-        const uint32_t bytes = pw < pg ? 128u * (uint32_t)h : 16u * (uint32_t)blk_diag_chunks(h);
         mbar_expect_tx(&bars[pstage], bytes);
-        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes,
-                  p.sstar + (p.s_begin + ps) * p.stride + blk_block_off(pg, pw, h), bytes, &bars[pstage]);
+        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes, psrc, bytes, &bars[pstage]);
       }
+      psrc += bytes >> 2;
     } else if (lane == 0) {
 #ifdef CM_EXP_L2INPUT
       const int z = (int)((p.s_begin + ps) & 63);                   // timing experiment
@@ -449,6 +479,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         ps = hk.next(ps);
         if (lane == 0) sq[qhead & 7] = ps;
         ++qhead;
+        if (BLK && ps < p.s_count) psrc = p.sstar + (p.s_begin + ps) * p.stride;
       }
     }
   };
@@ -464,14 +495,15 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     uint32_t* out = hk.begin(s);
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
-      // BLK diagonal block: chunk c of this lane's row at byte 16 lane + dgo[c] of the stage
+      // BLK diagonal block: chunk c of this lane's row at byte dgo[c] of the stage,
+      // 16 (B_c + lane - 4c) for the rows that have chunk c (lane >= 4c), 0 for the others
       uint32_t dgo[8];
       if (BLK) {
-        const int h = blk_rows(p.n, g);
+        const int h = g == Gr - 1 ? h_last : 32;
         int b = 0;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          dgo[c] = 16u * (uint32_t)(b - 4 * c);
+          dgo[c] = lane >= 4 * c ? 16u * (uint32_t)(b + lane - 4 * c) : 0u;
           b += max(0, h - 4 * c);
         }
       }
@@ -487,19 +519,25 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         // (BLK: off-diagonal blocks are stored in the tile's swizzled form; the diagonal block
         // chunk-major, so a quarter-warp's 16-byte reads of one chunk are consecutive)
         const bool pitched = pitched_of(s);
-        const bool bdiag = BLK && w == g;
-        const uint32_t rb = tiles_u32 + (uint32_t)cstage * kStageBytes +
-                            (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : bdiag ? 16u : 128u);
+        const uint32_t st0 = tiles_u32 + (uint32_t)cstage * kStageBytes;
+        const uint32_t rb = st0 + (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : 128u);
         const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
+        uint64_t xp[16];                                            // elements (2k, 2k+1) of the row
+        if (BLK && w == g) {                                        // (rows l < 4c have no chunk c: any
+#pragma unroll                                                      //  in-stage address, the bits are masked)
+          for (int c = 0; c < 8; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(st0 + dgo[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                         : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + (((uint32_t)c << 4) ^ sw)));
+        }
         float x[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float4 v;
-          // (rows l < 4c have no chunk c: any in-stage address will do, the bits are masked)
-          const uint32_t off = bdiag ? (lane >= 4 * c ? dgo[c] : 0u) : (((uint32_t)c << 4) ^ sw);
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(rb + off));
-          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        for (int k = 0; k < 16; ++k) {
+          x[2 * k] = __uint_as_float((uint32_t)xp[k]);
+          x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
         }
         cstage = cstage + 1 == kSt ? 0 : cstage + 1;
         // Row word of this lane's row r = rq over block w: bit q = S_{r, 32w+q} = [x_q > theta]
@@ -543,13 +581,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
           for (int j = 0; j < NT; ++j) word[j] = rw[j] & rmask;
         } else {
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            // two independent chains of (FSETP, predicated add): 2 instructions per element
-            uint32_t lo = 0u, hi = 0u;
-            pack_gt<0>(lo, x, th[j]);
-            pack_gt<16>(hi, x, th[j]);
-            word[j] = (lo | hi) & rmask;
-          }
+          for (int j = 0; j < NT; ++j) word[j] = pack_sub(xp, tt[j]) & rmask;
         }
         const int node = 32 * w + lane;
         const int brow_at = p.brow + (g + 1) * G + w;               // row 32(g+1) = lane 31's row

@@ -136,6 +136,25 @@ def test_rounding_edge_values(layout):
     compare(g, x, [0.5, 0.0, 1.0, np.nextafter(np.float32(0.5), np.float32(0))], masks=True, layout=layout)
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_rounding_ieee_corners(layout):
+    """The packed-fp32 compare (sign of theta - x) against IEEE '>' on the corners:
+    +-0 with theta = +-0, denormals next to a denormal / zero theta, +-inf, quiet and signalling
+    NaNs of both signs, values one ulp either side of theta."""
+    g = G.random_training(12, 0.2, 6)
+    n = g.n
+    bits = np.array([0x00000000, 0x80000000, 0x00000001, 0x80000001, 0x00000002, 0x7F800000, 0xFF800000,
+                     0x7FC00000, 0xFFC00000, 0x7F800001, 0xFF800001, 0x3F000000, 0x3EFFFFFF, 0x3F000001,
+                     0x3F800000, 0x00800000, 0x007FFFFF], np.uint32)
+    vals = bits.view(np.float32)
+    x = np.zeros((4, n, n), np.float32)
+    rng = np.random.default_rng(3)
+    for s in range(4):
+        x[s] = vals[rng.integers(0, len(vals), (n, n))]
+    thetas = np.array([0x00000000, 0x80000000, 0x00000001, 0x3F000000], np.uint32).view(np.float32)
+    compare(g, x, list(thetas), masks=True, layout=layout)
+
+
 def test_binary_patterns_closed_forms():
     from tests.oracle_helpers import S_all, S_chen, S_liveness, S_zero
     L = 16
