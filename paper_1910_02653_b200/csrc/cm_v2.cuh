@@ -479,7 +479,11 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         ps = hk.next(ps);
         if (lane == 0) sq[qhead & 7] = ps;
         ++qhead;
+#ifdef CM_EXP_L2INPUT
+        if (BLK && ps < p.s_count) psrc = p.sstar + ((p.s_begin + ps) & 63) * p.stride;   // timing experiment
+#else
         if (BLK && ps < p.s_count) psrc = p.sstar + (p.s_begin + ps) * p.stride;
+#endif
       }
     }
   };

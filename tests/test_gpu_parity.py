@@ -147,10 +147,11 @@ def test_rounding_ieee_corners(layout):
                      0x7FC00000, 0xFFC00000, 0x7F800001, 0xFF800001, 0x3F000000, 0x3EFFFFFF, 0x3F000001,
                      0x3F800000, 0x00800000, 0x007FFFFF], np.uint32)
     vals = bits.view(np.float32)
-    x = np.zeros((4, n, n), np.float32)
+    ld = roundup4(n)
+    x = np.zeros((4, n, ld), np.float32)
     rng = np.random.default_rng(3)
     for s in range(4):
-        x[s] = vals[rng.integers(0, len(vals), (n, n))]
+        x[s] = vals[rng.integers(0, len(vals), (n, ld))]
     thetas = np.array([0x00000000, 0x80000000, 0x00000001, 0x3F000000], np.uint32).view(np.float32)
     compare(g, x, list(thetas), masks=True, layout=layout)
 
