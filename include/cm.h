@@ -51,10 +51,11 @@ typedef enum {
                                  row group g = rows 32g+1 .. 32g+h_g, h_g = min(32, n-1-32g), g = 0..Gr-1,
                                  Gr = ceil((n-1)/32); blocks w = 0..g (nodes 32w .. 32w+31) stored group
                                  after group, block after block, block (g, w) at float offset
-                                 4 (128 g (g-1) + 144 g) + 32 h_g w.  Off-diagonal block (w < g): h_g rows
-                                 x 32 floats, the 4-float chunk c of row l (nodes 32w+4c ..) at chunk
-                                 c XOR (l mod 8).  Diagonal block (w = g): chunk-major, chunk c of rows
-                                 l = 4c .. h_g-1 at chunk B_c + l - 4c, B_c = sum_{c'<c} max(0, h_g - 4c').
+                                 4 (128 g (g-1) + 144 g) + 32 h_g w, each chunk-major in 4-float chunks
+                                 (chunk c of row l = nodes 32w+4c .. 32w+4c+3 of row 32g+1+l):
+                                 off-diagonal block (w < g): chunk c of row l at chunk h_g c + l;
+                                 diagonal block (w = g): chunk c of rows l = 4c .. h_g-1 at chunk
+                                 B_c + l - 4c, B_c = sum_{c'<c} max(0, h_g - 4c').
                                  Entries with i >= t inside a stored chunk are never read.
                                  cm_sstar_floats gives the size. */
 #define CM_KEY_NONE INT64_MAX /* best_key value meaning "no feasible candidate" */

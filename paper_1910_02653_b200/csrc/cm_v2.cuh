@@ -71,10 +71,12 @@ __device__ __forceinline__ int64_t row_offset(int layout, int64_t ld, int r) {
 
 // CM_LAYOUT_BLK, the blocked strict lower triangle (include/cm.h): row group g = rows
 // 32g+1 .. 32g+h_g (h_g = min(32, n-1-32g)), blocks w = 0..g of 32 nodes, stored group after
-// group, block after block; an off-diagonal block is h_g rows x 32 floats with 16-byte chunk c
-// of row l at chunk c ^ (l & 7) (the 128-byte swizzle of the K1 tile), the diagonal block
-// chunk-major: chunk c of rows l = 4c .. h_g-1.  Every group but the last is full (h = 32):
-// 128 g (g-1) + 144 g chunks precede group g.
+// group, block after block, every block chunk-major (16-byte chunk c = nodes 32w+4c .. +3):
+// off-diagonal blocks chunk c of row l at chunk h_g c + l, the diagonal block chunk c of rows
+// l = 4c .. h_g-1 at chunk B_c + l - 4c.  So K1 lane l reads chunk c at 16 l + a per-chunk
+// constant (an immediate offset for the full groups), and a quarter-warp's reads of one chunk
+// are 8 consecutive 16-byte units (no bank conflict).  Every group but the last is full
+// (h = 32): 128 g (g-1) + 144 g chunks precede group g.
 __host__ __device__ __forceinline__ int blk_rows(int n, int g) { return min(32, n - 1 - 32 * g); }
 __host__ __device__ __forceinline__ int blk_diag_chunks(int h) {
   int c = 0;
@@ -128,7 +130,8 @@ struct Transposer {
     for (int k = 0; k < 5; ++k) {
       const uint32_t y = __shfl_xor_sync(FULL, x, 16 >> k);
       const uint32_t t = __funnelshift_l(y, y, sh[k]);
-      x = (x & K[k]) | (t & ~K[k]);
+      // x = (x & K) | (t & ~K) as ONE lop3 (left to itself ptxas splits it into three)
+      asm("lop3.b32 %0, %0, %1, %2, 0xE4;" : "+r"(x) : "r"(t), "r"(K[k]));
     }
     return x;
   }
@@ -499,16 +502,17 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     uint32_t* out = hk.begin(s);
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
-      // BLK diagonal block: chunk c of this lane's row at byte dgo[c] of the stage,
-      // 16 (B_c + lane - 4c) for the rows that have chunk c (lane >= 4c), 0 for the others
+      // BLK, partial last group (h_last < 32): diagonal chunk c of this lane's row at byte dgo[c]
+      // of the stage, 16 (B_c + lane - 4c) for the rows that have chunk c (lane >= 4c), 0 for
+      // the others (any in-stage address: their bits are masked)
+      const bool bfull = !BLK || g < Gr - 1 || h_last == 32;
       uint32_t dgo[8];
-      if (BLK) {
-        const int h = g == Gr - 1 ? h_last : 32;
+      if (BLK && !bfull) {
         int b = 0;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           dgo[c] = lane >= 4 * c ? 16u * (uint32_t)(b + lane - 4 * c) : 0u;
-          b += max(0, h - 4 * c);
+          b += max(0, h_last - 4 * c);
         }
       }
       int64_t mass[NT];
@@ -527,10 +531,27 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         const uint32_t rb = st0 + (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : 128u);
         const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
         uint64_t xp[16];                                            // elements (2k, 2k+1) of the row
-        if (BLK && w == g) {                                        // (rows l < 4c have no chunk c: any
-#pragma unroll                                                      //  in-stage address, the bits are masked)
-          for (int c = 0; c < 8; ++c)
-            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(st0 + dgo[c]));
+        if (BLK) {
+          const uint32_t rb16 = st0 + 16u * (uint32_t)lane;
+          if (bfull && w == g) {                                    // chunk-major diagonal, h = 32:
+            constexpr uint32_t kDiag[8] = {0, 448, 832, 1152, 1408, 1600, 1728, 1792};   // 16 (B_c - 4c)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + kDiag[c]));
+          } else if (bfull) {                                       // chunk-major 32-row block
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + 512u * c));
+          } else if (w == g) {                                      // partial diagonal (rows l < 4c
+#pragma unroll                                                      //  read any in-stage address)
+            for (int c = 0; c < 8; ++c)
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(st0 + dgo[c]));
+          } else {                                                  // partial block: chunk stride h_last
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                           : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + 16u * (uint32_t)h_last * c));
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 8; ++c)
@@ -1328,14 +1349,22 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// lane 0 waits until *p >= target (then the warp proceeds); exponential back-off sleep
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// lane 0 waits until *p >= target (then the warp proceeds); exponential back-off sleep.  The
+// counters only grow: poll with relaxed loads (an acquire load invalidates L1 -- CCTL.IVALL --
+// every time) and acquire once when the target is reached.
 __device__ __forceinline__ void warp_wait_geq(const uint32_t* p, uint32_t target) {
   if ((threadIdx.x & 31) == 0) {
     uint32_t ns = 32;
-    while (ld_acquire(p) < target) {
+    while (ld_relaxed(p) < target) {
       __nanosleep(ns);
       ns = ns < 1024 ? 2 * ns : ns;
     }
+    (void)ld_acquire(p);
   }
   __syncwarp();
 }

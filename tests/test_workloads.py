@@ -137,9 +137,9 @@ def test_blk_layout_small_case_by_hand():
     assert dict(zip(zip(r.tolist(), i.tolist()), pos.tolist()))[(3, 2)] == 4 * 2 + 2
 
 
-def test_blk_layout_offdiagonal_swizzle():
-    """n = 40: group 1 holds rows 33..39 (h = 7); its block w = 0 is 7 rows x 32 floats with
-    chunk c of row l at chunk c ^ l; group 0's 32 x 32 diagonal block (576 floats) precedes it."""
+def test_blk_layout_offdiagonal_chunk_major():
+    """n = 40: group 1 holds rows 33..39 (h = 7); its block w = 0 is chunk-major, chunk c of row
+    l at chunk 7 c + l; group 0's 32 x 32 diagonal block (576 floats) precedes it."""
     from workloads.sstar import dense_to_blk
     x = np.zeros((1, 40, 40), np.float32)
     for r in range(40):
@@ -149,5 +149,5 @@ def test_blk_layout_offdiagonal_swizzle():
     base = 576
     for l in range(7):
         for c in range(8):
-            assert list(b[base + 32 * l + 4 * (c ^ l): base + 32 * l + 4 * (c ^ l) + 4]) == \
-                [1000 * (33 + l) + 4 * c + e for e in range(4)]
+            o = base + 4 * (7 * c + l)
+            assert list(b[o:o + 4]) == [1000 * (33 + l) + 4 * c + e for e in range(4)]

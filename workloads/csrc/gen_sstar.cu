@@ -28,7 +28,7 @@ __device__ __forceinline__ int64_t blk_pos(int n, int r, int i) {
   const int g = (r - 1) >> 5, l = (r - 1) & 31, w = i >> 5, q = i & 31, c = q >> 2, e = q & 3;
   const int h = min(32, n - 1 - 32 * g);
   const int64_t base = 4 * (128 * (int64_t)g * (g - 1) + 144 * (int64_t)g) + (int64_t)32 * h * w;
-  if (w < g) return base + 32 * l + 4 * (c ^ (l & 7)) + e;
+  if (w < g) return base + 4 * (h * c + l) + e;
   int b = 0;
   for (int k = 0; k < c; ++k) b += max(0, h - 4 * k);
   return base + 4 * (b + l - 4 * c) + e;

@@ -171,15 +171,15 @@ def blk_size(n: int) -> int:
 def blk_positions(n: int):
     """(rows, cols, positions): the float position of every strict-lower entry (r, i) in the
     blocked layout: row group g = (r-1) div 32, row l = (r-1) mod 32 of it, block w = i div 32;
-    off-diagonal blocks row-major with 16-byte chunk c of row l at chunk c ^ (l mod 8), the
-    diagonal block chunk-major (chunk c of rows l = 4c .. h-1)."""
+    every block chunk-major (16-byte chunk c = nodes 32w+4c .. +3): off-diagonal chunk c of
+    row l at chunk h c + l, diagonal chunk c of rows l = 4c .. h-1 at chunk B_c + l - 4c."""
     r, i = np.tril_indices(n, -1)
     g, l = (r - 1) // 32, (r - 1) % 32
     w, q = i // 32, i % 32
     c, e = q // 4, q % 4
     h = np.minimum(32, n - 1 - 32 * g)
     base = 4 * (128 * g * (g - 1) + 144 * g) + 32 * h * w
-    off = base + 32 * l + 4 * (c ^ (l % 8)) + e
+    off = base + 4 * (h * c + l) + e
     bc = np.zeros_like(c)
     for k in range(8):
         bc += np.where(k < c, np.maximum(0, h - 4 * k), 0)
