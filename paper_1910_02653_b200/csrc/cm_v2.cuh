@@ -317,8 +317,10 @@ __host__ __device__ constexpr size_t k1_bar_off(int nt, bool bulk = false) {
 __host__ __device__ constexpr size_t k1_cols_off(int nt, bool bulk = false) {
   return k1_bar_off(nt, bulk) + (size_t)k1_warps(nt) * k1_stages(nt) * 8;
 }
+// (512-byte aligned: a block's 8 x 16-entry int32 table is one 512-byte run, so an entry's
+// address is table | (nibble << 2) plus an immediate 64 q -- one LOP3 per lookup)
 __host__ __device__ constexpr size_t k1_nib_off(int nt, bool bulk = false) {
-  return k1_cols_off(nt, bulk) + (size_t)k1_warps(nt) * nt * 128;
+  return (k1_cols_off(nt, bulk) + (size_t)k1_warps(nt) * nt * 128 + 511) & ~(size_t)511;
 }
 // dynamic bytes to request: + 1024 slack for aligning the base
 __host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries, bool bulk = false) {
@@ -516,8 +518,9 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         }
       }
       int64_t mass[NT];
+      int32_t mass32[NT];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) mass[j] = 0;
+      for (int j = 0; j < NT; ++j) mass[j] = 0, mass32[j] = 0;
       for (int w = 0; w <= g; ++w) {
         issue();
         mbar_wait(&bars[cstage], (phase_bits >> cstage) & 1u);
@@ -617,17 +620,23 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
           oj[grp_off(g) + node] = transpose(word[j]);               // node 32w+lane's column: bit b = row 32g+1+b
         }
 #ifndef CM_EXP_NOMASS                                               // timing experiment: no masses
-        if (scaled32) {                                             // scaled masses fit int32
-          const unsigned char* tb = reinterpret_cast<const unsigned char*>(nib32 + 128 * w);
+        if (scaled32) {                                             // scaled masses fit int32 (every row's)
+          const uint32_t tb = smem_u32(nib32) + 512u * (uint32_t)w;   // 512-byte aligned
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
-            int32_t m32 = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint32_t off = q == 0 ? (word[j] << 2) & 0x3Cu : (word[j] >> (4 * q - 2)) & 0x3Cu;
-              m32 += *reinterpret_cast<const int32_t*>(tb + 64 * q + off);
-            }
-            mass[j] += m32;
+            int32_t v[8];
+            const uint32_t wd = word[j];
+            // entry address (nibble << 2) | table: one LOP3 ((a & 0x3C) | c, LUT 0xEA) per lookup
+            auto ent = [&](uint32_t sh) {
+              uint32_t a;
+              asm("lop3.b32 %0, %1, 0x3C, %2, 0xEA;" : "=r"(a) : "r"(sh), "r"(tb));
+              return a;
+            };
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[0]) : "r"(ent(wd << 2)));
+#define CM_NIB(Q) asm volatile("ld.shared.u32 %0, [%1+" #Q "*64];" : "=r"(v[Q]) : "r"(ent(wd >> (4 * Q - 2))))
+            CM_NIB(1); CM_NIB(2); CM_NIB(3); CM_NIB(4); CM_NIB(5); CM_NIB(6); CM_NIB(7);
+#undef CM_NIB
+            mass32[j] += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
           }
         } else {
           const int64_t* tw = p.nib + 128 * w;
@@ -644,7 +653,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
       if (rq < p.n) {
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          if (scaled32) reinterpret_cast<int32_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = (int32_t)mass[j];
+          if (scaled32) reinterpret_cast<int32_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass32[j];
           else reinterpret_cast<int64_t*>(out + (int64_t)j * p.cs + p.bw)[rq] = mass[j];
         }
       }
