@@ -31,7 +31,13 @@ LIBS = {
         [],
         [],
     ),
-    # measurement tool (integer-pipe roofline, tools/int_peak.py), not the product
+    # measurement tools (integer-pipe roofline, tools/int_peak.py; HBM read ceiling of the
+    # bulk-copy pattern, tools/bw_probe.py), not the product
+    os.path.join(ROOT, "tools", "libcm_bwprobe.so"): (
+        [os.path.join(ROOT, "tools", "csrc", "bw_probe.cu")],
+        [],
+        [],
+    ),
     os.path.join(ROOT, "tools", "libcm_intpeak.so"): (
         [os.path.join(ROOT, "tools", "csrc", "int_peak.cu")],
         [],
