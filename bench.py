@@ -448,17 +448,19 @@ def main():
     # ---- e2e through the public API with HOST buffers (rank-local, then the same MIN) ----
     e2e = None
     if not a.no_e2e and not a.samples:
-        # e2e through the public API: pinned HOST buffers in the packed tri4 layout (half the
-        # PCIe bytes of dense); H2D copies, kernels and D2H of peak/cost/keys all timed.
+        # e2e through the public API: pinned HOST buffers in a packed triangle layout (the
+        # timed run's blocked layout, or tri4 when that one is dense: half the PCIe bytes of
+        # dense); H2D copies, kernels and D2H of peak/cost/keys all timed.
         eb = min(a.e2e_batch, batch)
-        egen = DeviceGenerator(g, fam, seed, layout="tri4")
+        elay = a.layout if a.layout in ("blk", "tri4") else "tri4"
+        egen = DeviceGenerator(g, fam, seed, layout=elay)
         staging = torch.empty(egen.shape(eb), dtype=torch.float32, device=dev)
         egen.fill(staging, s_base)
         host = torch.empty((eb, egen.stride), dtype=torch.float32, pin_memory=True)
         host.copy_(staging.view(eb, -1))
         del staging
         pipe = cm.HostPipeline(graph, egen.stride, chunk=2048, n_theta=n_theta, n_budget=len(budgets),
-                               layout="tri4", device=dev)
+                               layout=elay, device=dev)
         pipe.run(host, th, bu, index_base=rank * eb * n_theta, total_candidates=world * eb * n_theta)
         torch.cuda.synchronize()
         e_steps = max(1, min(a.steps, 5))
@@ -480,7 +482,7 @@ def main():
         e2e = {"value": world * eb * n_theta * e_steps / e_dt, "unit": UNIT,
                "h2d_bytes_per_step": eb * egen.stride * 4,
                "d2h_bytes_per_step": eb * n_theta * 16 + 8 * len(budgets),
-               "batch_per_gpu": eb, "host_memory": "pinned", "layout": "tri4",
+               "batch_per_gpu": eb, "host_memory": "pinned", "layout": elay,
                "h2d_gb_per_s": eb * egen.stride * 4 * e_steps / e_dt / 1e9,
                "note": "PCIe-bound: the S* bytes cross the host link every step"}
 

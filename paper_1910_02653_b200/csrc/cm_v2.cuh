@@ -372,6 +372,234 @@ struct DiagMaps {
   CUtensorMap diag;    // box {32 nodes, 32 rows}, SWIZZLE_128B, no promotion
 };
 
+// a1 word of one 32 x 32 block (row r = rq of this lane, nodes 32w ..): randomized rounding
+// (R1): sample th0 + j of node i-1 = 32w + q in row rq is word q % 4 of the Philox
+// block with counter (8w + q / 4, rq, global S* index, th0 + j): one block per four
+// consecutive nodes and sample.  u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < t = ceil(x 2^24)
+// (exact in fp32; t clamped to [0, 2^24]: x > 1 or inf always, x <= 0 or NaN never)  <=>
+// w <= 256 t - 1 for t >= 1 (t = 2^24 wraps to 2^32 - 1: always); t = 0: never.
+template <int NT>
+__device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t (&xp)[16], int w, int rq, uint32_t sg,
+                                           const RoundParams& p) {
+  float x[32];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    x[2 * k] = __uint_as_float((uint32_t)xp[k]);
+    x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) word[j] = 0u;
+#pragma unroll
+  for (int q4 = 0; q4 < 8; ++q4) {
+    uint32_t tw[4], qb[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int q = 4 * q4 + e;
+      const float xs = x[q] * 16777216.0f;
+      const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
+      tw[e] = (t << 8) - 1u;
+      qb[e] = t != 0u ? (1u << q) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
+                                    p.key0, p.key1);
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) word[j] |= ow[e] <= tw[e] ? qb[e] : 0u;
+    }
+  }
+}
+
+// K1 for the blocked layout (CM_LAYOUT_BLK): the same per-block steps as k1_body, with the
+// bookkeeping hoisted out of the block loop -- a group's row masks, store pointers and table
+// base are set once per group (running pointers inside it), and the producer cursor is a
+// running source pointer whose block sizes follow from (pg, pw) alone.
+template <int NT, bool RAND, class Hooks>
+__device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char* k1smem, int wl, int* sq,
+                                            const Hooks& hk, int Gr) {
+  constexpr int kSt = k1_stages(NT);
+  constexpr uint32_t kStageBytes = 4096u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t tiles = smem_u32(k1smem) + (uint32_t)(kSt * kStageBytes) * (uint32_t)wl;
+  const uint32_t bars = smem_u32(k1smem + k1_bar_off(NT, false)) + 8u * (uint32_t)(kSt * wl);
+  const uint32_t nibs = smem_u32(k1smem + k1_nib_off(NT, false));
+  const int G = p.G, n = p.n;
+  const int64_t cs = p.cs;
+  uint64_t tt[NT];                                                  // theta (-0 -> +0) in both halves
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const uint32_t b = __float_as_uint(RAND ? 0.f : p.theta[p.th0 + j] + 0.0f);
+    tt[j] = ((uint64_t)b << 32) | b;
+  }
+  const Transposer transpose(lane);
+  const bool scaled32 = p.nib32 != nullptr;
+  // every group but the last (h_last rows) is full: 4 KB off-diagonal, 2 304-byte diagonal blocks
+  const int h_last = blk_rows(n, Gr - 1);
+  const uint32_t off_last = 128u * (uint32_t)h_last, diag_last = 16u * (uint32_t)blk_diag_chunks(h_last);
+
+  // ---- producer cursor (S* ps, block (pg, pw), stage pstage), kSt - 1 blocks ahead
+  int ps = hk.first(), pg = 0, pw = 0;
+  uint32_t pstage = 0;
+  unsigned qhead = 0, qtail = 0;                                    // sq ring (warp-uniform)
+  if (lane == 0) sq[0] = ps;
+  ++qhead;
+  const float* psrc = ps < p.s_count ? p.sstar + (p.s_begin + ps) * p.stride : p.sstar;
+  auto issue = [&]() {
+    if (ps >= p.s_count) return;
+    const bool last = pg == Gr - 1;
+    const uint32_t bytes = pw < pg ? (last ? off_last : 4096u) : (last ? diag_last : 2304u);
+    if (lane == 0) {
+      const uint32_t bar = bars + 8u * pstage;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   :: "r"(tiles + kStageBytes * pstage), "l"(psrc), "r"(bytes), "r"(bar) : "memory");
+    }
+    psrc += bytes >> 2;
+    pstage = pstage + 1 == (uint32_t)kSt ? 0u : pstage + 1;
+    if (++pw > pg) {
+      pw = 0;
+      if (++pg == Gr) {
+        pg = 0;
+        ps = hk.next(ps);
+        if (lane == 0) sq[qhead & 7] = ps;
+        ++qhead;
+        if (ps < p.s_count) psrc = p.sstar + (p.s_begin + ps) * p.stride;
+      }
+    }
+  };
+#pragma unroll
+  for (int d = 0; d < kSt - 1; ++d) issue();
+
+  // ---- consumer
+  uint32_t cstage = 0, cpar = 0;
+  auto wait_block = [&]() {                                         // returns the stage's smem address
+    issue();
+    const uint32_t bar = bars + 8u * cstage;
+    asm volatile("{\n\t.reg .pred p;\n\tWAITB_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAITB_%=;\n\t}" :: "r"(bar), "r"(cpar) : "memory");
+    const uint32_t st0 = tiles + kStageBytes * cstage;
+    if (++cstage == (uint32_t)kSt) {
+      cstage = 0;
+      cpar ^= 1u;
+    }
+    return st0;
+  };
+  for (;;) {
+    __syncwarp();
+    const int s = sq[qtail & 7];
+    ++qtail;
+    if (s >= p.s_count) break;
+    uint32_t* out = hk.begin(s);
+    const uint32_t sg = p.s0 + (uint32_t)(p.s_begin + s);           // RAND: global S* index
+    for (int g = 0; g < Gr; ++g) {
+      const int rq = 32 * g + lane + 1;                             // row owned by this lane
+      // row masks (a1 reads i < t only, rows < n): FULL off the diagonal, nodes 32g .. rq-1 on it
+      const uint32_t rm_off = rq < n ? FULL : 0u;
+      const uint32_t rm_diag = rq < n ? (lane == 31 ? FULL : (2u << lane) - 1u) : 0u;
+      uint32_t* colp = out + grp_off(g) + lane;                     // node 32w+lane's column word
+      uint32_t* browp = out + p.brow + (g + 1) * G;                 // row 32(g+1) = lane 31's row
+      const bool wbrow = lane == 31 && g + 1 < G;
+      uint32_t tb = nibs;                                           // block w's mass table
+      int32_t mass32[NT];
+      int64_t mass[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) mass32[j] = 0, mass[j] = 0;
+      // one block: xp holds this lane's row (elements 2k, 2k+1 in xp[k]), w its node block
+      auto block = [&](const uint64_t (&xp)[16], uint32_t rmask, int w) {
+        uint32_t word[NT];
+        if (RAND) {
+          rand_words<NT>(word, xp, w, rq, sg, p);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) word[j] &= rmask;
+        } else {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) word[j] = pack_sub(xp, tt[j]) & rmask;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          if (wbrow) browp[j * cs] = word[j];
+          colp[j * cs] = transpose(word[j]);                        // bit b = row 32g+1+b
+        }
+        ++browp;
+        colp += 32;
+#ifndef CM_EXP_NOMASS
+        if (scaled32) {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            int32_t v[8];
+            const uint32_t wd = word[j];
+            auto ent = [&](uint32_t sh) {                           // (nibble << 2) | table: one LOP3
+              uint32_t a;
+              asm("lop3.b32 %0, %1, 0x3C, %2, 0xEA;" : "=r"(a) : "r"(sh), "r"(tb));
+              return a;
+            };
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[0]) : "r"(ent(wd << 2)));
+#define CM_NIB(Q) asm volatile("ld.shared.u32 %0, [%1+" #Q "*64];" : "=r"(v[Q]) : "r"(ent(wd >> (4 * Q - 2))))
+            CM_NIB(1); CM_NIB(2); CM_NIB(3); CM_NIB(4); CM_NIB(5); CM_NIB(6); CM_NIB(7);
+#undef CM_NIB
+            mass32[j] += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+          }
+        } else {
+          const int64_t* tw64 = p.nib + 128 * w;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            int64_t ms = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ms += __ldg(tw64 + 16 * q + ((word[j] >> (4 * q)) & 15u));
+            mass[j] += ms;
+          }
+        }
+#endif
+        tb += 512u;
+      };
+      // one body for every block (the hot loop stays small next to K2's in the instruction
+      // cache); only the 8 shared loads depend on the block's form
+      const bool bfull = g < Gr - 1 || h_last == 32;
+      for (int w = 0; w <= g; ++w) {
+        const uint32_t st0 = wait_block();
+        const uint32_t rb = st0 + 16u * (uint32_t)lane;
+        uint64_t xp[16];
+        if (w < g && bfull) {                                       // chunk-major 32-row block
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + 512u * c));
+        } else if (bfull) {                                         // chunk-major diagonal, h = 32
+          constexpr uint32_t kDiag[8] = {0, 448, 832, 1152, 1408, 1600, 1728, 1792};   // 16 (B_c - 4c)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + kDiag[c]));
+        } else if (w < g) {                                         // partial group: chunk stride h_last
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                         : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + 16u * (uint32_t)h_last * c));
+        } else {
+          // partial diagonal: chunk c of this lane's row at byte 16 (B_c + lane - 4c) for the rows
+          // that have chunk c (lane >= 4c), any in-stage address for the others (bits masked)
+          int b = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t a = lane >= 4 * c ? st0 + 16u * (uint32_t)(b + lane - 4 * c) : st0;
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(a));
+            b += max(0, h_last - 4 * c);
+          }
+        }
+        block(xp, w < g ? rm_off : rm_diag, w);
+      }
+      if (rq < n) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          if (scaled32) reinterpret_cast<int32_t*>(out + (int64_t)j * cs + p.bw)[rq] = mass32[j];
+          else reinterpret_cast<int64_t*>(out + (int64_t)j * cs + p.bw)[rq] = mass[j];
+        }
+      }
+    }
+    hk.end(s);
+  }
+}
+
 // K1 body of one warp: S* s = hk.first(), hk.next(s), ... while < s_count; wl = the warp's
 // index among the CTA's K1 warps (its stage ring).  The TMA cursor runs ahead of the
 // consumer and may enter the next S* (or several, for tiny graphs) first: the S* indices it
@@ -383,7 +611,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
                                         unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
   constexpr bool BULK = LAY == 1;                                   // tri4
-  constexpr bool BLK = LAY == 2;                                    // blocked triangle (CM_LAYOUT_BLK)
+  constexpr bool BLK = LAY == 2;                                    // blocked triangle: k1_body_blk
   constexpr int kSt = k1_stages(NT);
   constexpr uint32_t kStageBytes = (uint32_t)k1_stage_bytes(BULK);
   int32_t* nib32 = reinterpret_cast<int32_t*>(k1smem + k1_nib_off(NT, BULK));   // p.nib32 staged (if any)
@@ -396,6 +624,10 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   const int Gr = p.n >= 2 ? (p.n - 2) / 32 + 1 : 0;
   if (Gr == 0) {
     for (int s = hk.first(); s < p.s_count; s = hk.next(s)) { hk.begin(s); hk.end(s); }
+    return;
+  }
+  if constexpr (BLK) {
+    k1_body_blk<NT, RAND>(p, k1smem, wl, sq, hk, Gr);
     return;
   }
   uint64_t tt[NT];                                                  // theta (-0 -> +0) in both halves
@@ -421,11 +653,6 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
   unsigned qhead = 0, qtail = 0;                                    // sq ring (warp-uniform)
   if (lane == 0) sq[0] = ps;
   ++qhead;
-  // BLK: the blocks are read in storage order, so the source is a running pointer; every group
-  // but the last (h_last rows) is full: 4 KB off-diagonal, 2 304-byte diagonal blocks
-  const int h_last = BLK ? blk_rows(p.n, Gr - 1) : 32;
-  const uint32_t diag_last = BLK ? 16u * (uint32_t)blk_diag_chunks(h_last) : 0u;
-  const float* psrc = BLK && ps < p.s_count ? p.sstar + (p.s_begin + ps) * p.stride : p.sstar;
   auto issue = [&]() {
     if (ps >= p.s_count) return;
     if (BULK && !pitched_of(ps)) {
@@ -454,16 +681,6 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes + (uint32_t)lane * kBulkPitch, src, 4u * (uint32_t)len,
                   &bars[pstage]);
       }
-    } else if (BLK) {
-      // blocked triangle: block (pg, pw) is one contiguous run of the S* -- one 1-D bulk copy
-      // (UBLKCP) of exactly its stored bytes, already in the stage's read form
-      const bool last = pg == Gr - 1;
-      const uint32_t bytes = pw < pg ? (last ? 128u * (uint32_t)h_last : 4096u) : (last ? diag_last : 2304u);
-      if (lane == 0) {
-        mbar_expect_tx(&bars[pstage], bytes);
-        bulk_load(tiles_u32 + (uint32_t)pstage * kStageBytes, psrc, bytes, &bars[pstage]);
-      }
-      psrc += bytes >> 2;
     } else if (lane == 0) {
 #ifdef CM_EXP_L2INPUT
       const int z = (int)((p.s_begin + ps) & 63);                   // timing experiment
@@ -484,11 +701,6 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         ps = hk.next(ps);
         if (lane == 0) sq[qhead & 7] = ps;
         ++qhead;
-#ifdef CM_EXP_L2INPUT
-        if (BLK && ps < p.s_count) psrc = p.sstar + ((p.s_begin + ps) & 63) * p.stride;   // timing experiment
-#else
-        if (BLK && ps < p.s_count) psrc = p.sstar + (p.s_begin + ps) * p.stride;
-#endif
       }
     }
   };
@@ -504,19 +716,6 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     uint32_t* out = hk.begin(s);
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
-      // BLK, partial last group (h_last < 32): diagonal chunk c of this lane's row at byte dgo[c]
-      // of the stage, 16 (B_c + lane - 4c) for the rows that have chunk c (lane >= 4c), 0 for
-      // the others (any in-stage address: their bits are masked)
-      const bool bfull = !BLK || g < Gr - 1 || h_last == 32;
-      uint32_t dgo[8];
-      if (BLK && !bfull) {
-        int b = 0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          dgo[c] = lane >= 4 * c ? 16u * (uint32_t)(b + lane - 4 * c) : 0u;
-          b += max(0, h_last - 4 * c);
-        }
-      }
       int64_t mass[NT];
       int32_t mass32[NT];
 #pragma unroll
@@ -527,46 +726,15 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         phase_bits ^= 1u << cstage;
         // this lane's row in the stage: the 144-byte-pitch per-row form (tri4 fallback) or the
         // 128-byte-swizzled 32 x 32 tile
-        // (BLK: off-diagonal blocks are stored in the tile's swizzled form; the diagonal block
-        // chunk-major, so a quarter-warp's 16-byte reads of one chunk are consecutive)
         const bool pitched = pitched_of(s);
         const uint32_t st0 = tiles_u32 + (uint32_t)cstage * kStageBytes;
         const uint32_t rb = st0 + (uint32_t)lane * (pitched ? (uint32_t)kBulkPitch : 128u);
         const uint32_t sw = pitched ? 0u : (uint32_t)(lane & 7) << 4;
         uint64_t xp[16];                                            // elements (2k, 2k+1) of the row
-        if (BLK) {
-          const uint32_t rb16 = st0 + 16u * (uint32_t)lane;
-          if (bfull && w == g) {                                    // chunk-major diagonal, h = 32:
-            constexpr uint32_t kDiag[8] = {0, 448, 832, 1152, 1408, 1600, 1728, 1792};   // 16 (B_c - 4c)
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + kDiag[c]));
-          } else if (bfull) {                                       // chunk-major 32-row block
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + 512u * c));
-          } else if (w == g) {                                      // partial diagonal (rows l < 4c
-#pragma unroll                                                      //  read any in-stage address)
-            for (int c = 0; c < 8; ++c)
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(st0 + dgo[c]));
-          } else {                                                  // partial block: chunk stride h_last
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
-                           : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb16 + 16u * (uint32_t)h_last * c));
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
-                         : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + (((uint32_t)c << 4) ^ sw)));
-        }
-        float x[32];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          x[2 * k] = __uint_as_float((uint32_t)xp[k]);
-          x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
-        }
+        for (int c = 0; c < 8; ++c)
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(xp[2 * c]), "=l"(xp[2 * c + 1]) : "r"(rb + (((uint32_t)c << 4) ^ sw)));
         cstage = cstage + 1 == kSt ? 0 : cstage + 1;
         // Row word of this lane's row r = rq over block w: bit q = S_{r, 32w+q} = [x_q > theta]
         // (a1: strict fp32 '>', NaN -> 0), masked to the strict lower triangle (32w+q < r) and
@@ -575,38 +743,9 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
         const uint32_t rmask = rq >= p.n ? 0u : (rem >= 32 ? FULL : (1u << rem) - 1u);
         uint32_t word[NT];
         if (RAND) {                                                 // a1 randomized: u < S*
-          // DESIGN.md R1: sample th0 + j of node i-1 = 32w + q in row rq is word q % 4 of the
-          // Philox block with counter (8w + q / 4, rq, global S* index, th0 + j): one block per
-          // four consecutive nodes and sample
-          uint32_t rw[NT];
+          rand_words<NT>(word, xp, w, rq, p.s0 + (uint32_t)(p.s_begin + s), p);
 #pragma unroll
-          for (int j = 0; j < NT; ++j) rw[j] = 0u;
-          const uint32_t sg = p.s0 + (uint32_t)(p.s_begin + s);
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            // u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < t = ceil(x 2^24) (exact in fp32; t clamped
-            // to [0, 2^24]: x > 1 or inf always, x <= 0 or NaN never)  <=>  w <= 256 t - 1 for
-            // t >= 1 (t = 2^24 wraps to 2^32 - 1: always); t = 0: never
-            uint32_t tw[4], qb[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int q = 4 * q4 + e;
-              const float xs = x[q] * 16777216.0f;
-              const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
-              tw[e] = (t << 8) - 1u;
-              qb[e] = t != 0u ? (1u << q) : 0u;
-            }
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
-                                            p.key0, p.key1);
-              const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) rw[j] |= ow[e] <= tw[e] ? qb[e] : 0u;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < NT; ++j) word[j] = rw[j] & rmask;
+          for (int j = 0; j < NT; ++j) word[j] &= rmask;
         } else {
 #pragma unroll
           for (int j = 0; j < NT; ++j) word[j] = pack_sub(xp, tt[j]) & rmask;
@@ -767,21 +906,46 @@ struct AView {
 // four-wide rounds.  x excludes the diagonal stage t = k: that compute is the first event of
 // stage t in the walk (R_{t,k} = 0 for k > t), so it always leaves E_t = M_t and the scan
 // initialises E with it instead.
+// E[stage][lane] is addressed in the shared window: eaddr = &E[0][lane], stage b at eaddr +
+// 32 b sizeof(ET).  A slot takes bit b = bfind(x) (0xffffffff when x = 0) and sel = 1 << b (0
+// then: a shift by 32 or more clears the word), so an empty slot needs no select; its load and
+// store are predicated off by sel = 0.
+template <typename ET>
+__device__ __forceinline__ void lds_if(ET& v, uint32_t addr, uint32_t sel) {
+  if constexpr (sizeof(ET) == 4)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+                 : "+r"(v) : "r"(addr), "r"(sel) : "memory");
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u64 %0, [%1];\n\t}"
+                 : "+l"(v) : "r"(addr), "r"(sel) : "memory");
+}
+template <typename ET>
+__device__ __forceinline__ void sts_if(uint32_t addr, uint32_t sel, ET v) {
+  if constexpr (sizeof(ET) == 4)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p st.shared.u32 [%0], %2;\n\t}"
+                 :: "r"(addr), "r"(sel), "r"(v) : "memory");
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p st.shared.u64 [%0], %2;\n\t}"
+                 :: "r"(addr), "r"(sel), "l"(v) : "memory");
+}
 template <int W, int NM, typename ET>
 __device__ __forceinline__ void event_round(uint32_t& x, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
-                                            ET* E, int lane) {
-  uint32_t sel[W];
-  int off[W];
+                                            uint32_t eaddr) {
+  uint32_t sel[W], addr[W];
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    const int b = 31 - __clz(x);                                    // -1 when x == 0
-    sel[u] = x != 0u ? 1u << b : 0u;
-    off[u] = 32 * (b & 31) + lane;
+    uint32_t b;
+    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(x));                   // highest set bit, ~0 if none
+    asm("shl.b32 %0, %1, %2;" : "=r"(sel[u]) : "r"(1u), "r"(b));   // 0 if none
+    addr[u] = eaddr + b * (uint32_t)(32 * sizeof(ET));
     x ^= sel[u];
   }
   ET ev[W];
 #pragma unroll
-  for (int u = 0; u < W; ++u) ev[u] = sel[u] ? E[off[u]] : (ET)0;
+  for (int u = 0; u < W; ++u) {
+    ev[u] = (ET)0;
+    lds_if(ev[u], addr[u], sel[u]);
+  }
 #pragma unroll
   for (int u = 0; u < W; ++u) {
     ET fr = (sf & sel[u]) ? Mk : (ET)0;
@@ -791,18 +955,18 @@ __device__ __forceinline__ void event_round(uint32_t& x, uint32_t sf, ET Mk, con
     ev[u] = max(ev[u] - fr, (ET)0) + Mk;                             // every term within [-sum M, sum M]
   }
 #pragma unroll
-  for (int u = 0; u < W; ++u)
-    if (sel[u]) E[off[u]] = ev[u];
+  for (int u = 0; u < W; ++u) sts_if(addr[u], sel[u], ev[u]);
 }
 template <int NM, typename ET>
 __device__ __forceinline__ void events(uint32_t x, uint32_t sf, ET Mk, const uint32_t* f, const ET* m,
                                        ET* E, int lane) {
   const unsigned mx = __reduce_max_sync(FULL, (unsigned)__popc(x));
   if (mx == 0) return;
-  if (mx == 1) event_round<1, NM, ET>(x, sf, Mk, f, m, E, lane);
-  else if (mx == 2) event_round<2, NM, ET>(x, sf, Mk, f, m, E, lane);
+  const uint32_t eaddr = smem_u32(E) + (uint32_t)(sizeof(ET) * lane);
+  if (mx == 1) event_round<1, NM, ET>(x, sf, Mk, f, m, eaddr);
+  else if (mx == 2) event_round<2, NM, ET>(x, sf, Mk, f, m, eaddr);
   else
-    while (__any_sync(FULL, x != 0u)) event_round<4, NM, ET>(x, sf, Mk, f, m, E, lane);
+    while (__any_sync(FULL, x != 0u)) event_round<4, NM, ET>(x, sf, Mk, f, m, eaddr);
 }
 
 // The far (non-adjacent) dependencies of node k (ndf of them, warp-uniform; three in
@@ -883,8 +1047,10 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
   uint4 n2quad = (lsn && (k0 >> 2) > 1) ? __ldcg(sn4 + (k0 >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
   // row 32g's word for k's 32-node block (blocks w < g only; nodes >= 32g are never in S_32g)
   // and, prefetched, for the block below
-  uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
+  const uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
   uint32_t bnext = (g > 0 && (k0 >> 5) >= 1 && live) ? __ldcg(brow + (k0 >> 5) - 1) : 0u;
+  uint32_t bcur = bword << (31 - (k0 & 31));                        // bit 31 = node k's bit of row 32g
+  uint32_t dg = 1u << (k0 - 32 * g);                                // e_t for k in 32g .. k0 (k0 >= 32g)
   int4 rec1 = nrec[k0];                                             // record of the next node
   // Sn_k: the previous step's Sn_{k-1}, so each step extracts one word of the quads
   uint32_t sn1 = (k0 & 3) == 3 ? quad.w : (k0 & 3) == 2 ? quad.z : (k0 & 3) == 1 ? quad.y : quad.x;
@@ -910,8 +1076,10 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
       sn1 = u == 0 ? nquad.w : c;
     }
     const uint32_t a = (rec.w >= 0 ? bslot : sn) | acc;             // A'_k, complete
-    const uint32_t sw = (sn << 1) | ((bword >> (k & 31)) & 1u);     // S_t from S_{t+1} and row 32g
-    const uint32_t diag = ((k >> 5) == g) ? (1u << (k & 31)) : 0u;
+    const uint32_t sw = __funnelshift_l(bcur, sn, 1);               // S_t from S_{t+1} and row 32g
+    const uint32_t diag = dg;                                       // stage t = k of this group
+    dg >>= 1;
+    bcur <<= 1;
     const uint32_t Rk = (a & ~sw) | diag;                           // a2 seed + a3 closure
     if (RSTORE && live) rcol[k] = Rk;                               // verification output
     // base of A'_{k-1}: its slot (final: every far user j > k is done; the adjacent user k
@@ -942,7 +1110,7 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
       n2quad = (lsn && (k >> 2) >= 3) ? __ldcg(sn4 + (k >> 2) - 3) : make_uint4(0u, 0u, 0u, 0u);
     }
     if ((k & 31) == 0) {                                            // next node is in the block below
-      bword = bnext;
+      bcur = bnext;
       bnext = (g > 0 && (k >> 5) >= 2 && live) ? __ldcg(brow + (k >> 5) - 2) : 0u;
     }
   }
@@ -1423,6 +1591,19 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
   return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1023) & ~(size_t)1023;
 }
 
+// Register rebalance (setmaxnreg, whole warpgroups): more than 16 warps per CTA leave fewer than
+// 128 registers per thread at launch; the rounding warps then drop to CM_FUSED_K1_REGS (the K1
+// body needs ~72) and the scan warps grow by what they released -- an increase is served from
+// the CTA's own pool of released registers only (USETMAXREG.TRY_ALLOC.CTAPOOL spins until it
+// can be), so sum of increases <= sum of decreases, or the scan warps wait forever.
+#ifndef CM_FUSED_K1_REGS
+#define CM_FUSED_K1_REGS 72
+#endif
+__host__ __device__ constexpr int fused_launch_regs(int nt) { return (65536 / (32 * fused_warps(nt))) / 8 * 8; }
+__host__ __device__ constexpr int fused_k2_regs(int nt) {
+  return (fused_launch_regs(nt) + k1_warps(nt) * (fused_launch_regs(nt) - CM_FUSED_K1_REGS) / kFusedScanWarps) / 8 * 8;
+}
+
 // ET: the scan state (int32 when sum M / gcd < 2^31, else int64).
 template <int NT, int LAY, bool RAND, typename ET>
 __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
@@ -1466,7 +1647,11 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (fp.trace && threadIdx.x == 0) fp.trace[4 * blockIdx.x] = globaltimer();
 
+  constexpr bool kRebal = fused_warps(NT) > 16;
+  static_assert(!kRebal || (KF1 % 4 == 0 && kFusedScanWarps % 4 == 0 && !kK1High), "warpgroup roles");
+  static_assert(!kRebal || (CM_FUSED_K1_REGS <= fused_launch_regs(NT) && fused_k2_regs(NT) <= 256), "register pool");
   if (kK1High ? warp >= kFusedScanWarps : warp < KF1) {             // ---- rounding (K1) warps
+    if constexpr (kRebal) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(CM_FUSED_K1_REGS));
     __shared__ int sq[KF1][8];
     const int w1 = kK1High ? warp - kFusedScanWarps : warp;
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
@@ -1476,6 +1661,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     return;
   }
   // ---- scan (K2) warps
+  if constexpr (kRebal) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(fused_k2_regs(NT)));
   const int wk = warp - kFirstScanWarp;
   const ScanCtx<ET, true> x = scan_ctx<ET, true>(sp, k2smem, wk, tmem_base, kFusedTmemCols);
   const int G = sp.G;

@@ -1,7 +1,7 @@
 """GPU parity at scale and the cross-GPU argmin (a8) on CUDA-produced keys.
 
-- Each of bench.py's five configs at its exact bench launch (device-generated dense S* with
-  128-byte rows, bench's seed, fused persistent kernel, consecutive calls overlapped on two
+- Each of bench.py's five configs at its exact bench launch (device-generated S* in the
+  blocked layout bench.py times, and in the dense layout with 128-byte rows; bench's seed, fused persistent kernel, consecutive calls overlapped on two
   alternating output sets with in-kernel key init): >= 2 000 candidates per config checked
   against the CPU oracle -- the first 1 000, unit boundaries, the last unit and 1 000 random
   ones -- and every per-budget key against the call's own per-candidate outputs.  A second
@@ -66,16 +66,17 @@ def oracle_keys(peaks, costs, budgets, bits, index_base=0):
 
 
 @pytest.mark.timeout(1800)
+@pytest.mark.parametrize("layout", ["blk", "dense"])
 @pytest.mark.parametrize("cfg", ["resnet50", "vgg16", "unet", "mobilenet", "fcn8"])
-def test_bench_config_full_launch(cfg, env_var):
+def test_bench_config_full_launch(cfg, layout, env_var):
     import torch
     import paper_1910_02653_b200 as cm
     from workloads.device_gen import DeviceGenerator
     g, fam, thetas, budgets, N = bench.build_workload(cfg)
     nt = len(thetas)
     dev = torch.device("cuda:0")
-    ld = -(-g.n // 32) * 32                                         # bench.py's default dense rows
-    dg = DeviceGenerator(g, fam, BENCH_SEED, layout="dense", ld=ld)
+    ld = -(-g.n // 32) * 32 if layout == "dense" else None          # bench.py's dense rows: 128 bytes
+    dg = DeviceGenerator(g, fam, BENCH_SEED, layout=layout, ld=ld)
     buf = torch.empty(dg.shape(N), dtype=torch.float32, device=dev)
     dg.fill(buf, 0)
     graph = cm.Graph.from_workload(g)
@@ -87,14 +88,15 @@ def test_bench_config_full_launch(cfg, env_var):
     for step in range(3):                                           # bench's step, 3 calls back to back
         o = sets[step % 2]
         out = cm.round_and_evaluate(graph, buf, th, bu, best_key=o["key"], peak=o["peak"], cost=o["cost"],
-                                    index_base=0, total_candidates=N * nt, init_keys=True, overlap=True)
+                                    index_base=0, total_candidates=N * nt, init_keys=True, overlap=True,
+                                    layout=layout)
         assert cm.debug_last_launches() == 1                        # the fused persistent kernel
     torch.cuda.synchronize()
     bits = out["idx_bits"]
     got = [(o["peak"].cpu().numpy(), o["cost"].cpu().numpy(), o["key"].cpu().numpy()) for o in sets]
     # ring-race detector: every candidate of the fused launch equals the two-kernel pipeline
     env_var(CM_FUSED=0)
-    ref = cm.round_and_evaluate(graph, buf, th, bu, total_candidates=N * nt)
+    ref = cm.round_and_evaluate(graph, buf, th, bu, total_candidates=N * nt, layout=layout)
     torch.cuda.synchronize()
     assert cm.debug_last_launches() >= 3
     env_var(CM_FUSED=1)
