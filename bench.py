@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
     ap.add_argument("--family", default=None)
+    ap.add_argument("--thetas", default=None,
+                    help="comma-separated thresholds (deterministic rounding, N_theta <= 4 per pass) "
+                         "instead of the config's")
     ap.add_argument("--max-batch", action="store_true",
                     help="also run the max-batch epilogue (Eq. 13) per budget in the timed step")
     ap.add_argument("--samples", type=int, default=None,
@@ -242,6 +245,8 @@ def run_reference(a):
     if rank != 0:
         return 0
     g, fam, thetas, budgets, batch = build_workload(a.config, a.family)
+    if a.thetas:
+        thetas = [float(t) for t in a.thetas.split(",")]
     from oracle import Instance, evaluate
     from workloads.sstar import gen_sstar
     inst = Instance.from_graph(g)
@@ -308,6 +313,8 @@ def main():
             dist.init_process_group(backend)
 
     g, fam, thetas, budgets, batch = build_workload(a.config, a.family)
+    if a.thetas:
+        thetas = [float(t) for t in a.thetas.split(",")]
     if a.batch:
         batch = a.batch
     seed = BENCH_SEED

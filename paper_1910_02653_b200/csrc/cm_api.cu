@@ -172,7 +172,7 @@ EncodeTiledFn encode_tiled() {
 int64_t cand_bytes(int n, bool m32) { return 4 * (int64_t)cm2::cand_words(n, m32) + 16 * (int64_t)((n + 31) / 32); }
 size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
   const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
-  return (size_t)(s32 ? 4 * 32 * 32 * 2 : 8 * 32 * 32) + (size_t)4 * 32 * spill;   // E (+ staged int32 masses), spill
+  return (size_t)cm2::scan_e_bytes(s32) + (size_t)4 * 32 * spill;   // E (+ staged int32 masses), spill
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
 // launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).
@@ -496,6 +496,13 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, fn, threads, smemf);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy(fused_kernel)");
       if (occf >= 1) {
+        const int grid = g->sm_count;                                 // one CTA per SM (all 512 TMEM columns)
+        if (env_flag("CM_DEBUG", 0)) {
+          cudaFuncAttributes fa = {};
+          cudaFuncGetAttributes(&fa, fn);
+          std::fprintf(stderr, "cm: fused_kernel smem %zu (static %zu) threads %d regs %d occupancy %d grid %d ring %lld\n",
+                       smemf, fa.sharedSizeBytes, threads, fa.numRegs, occf, grid, (long long)R);
+        }
         cm2::FusedParams fp;
         rp.s_begin = 0;
         rp.s_count = a->n_sstar;
@@ -516,7 +523,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         fp.total_tasks = total_tasks;
         fp.win_units = (int32_t)win;
         fp.trace = nullptr;
-        if (env_flag("CM_TRACE", 0) == 2 && g->sm_count <= kTraceCtas) {
+        if (env_flag("CM_TRACE", 0) == 2 && grid <= kTraceCtas) {
           const size_t region = 4 * (size_t)kTraceCtas;
           if (!g_cta_trace && cudaMalloc(&g_cta_trace, sizeof(uint64_t) * region * kTraceCalls) != cudaSuccess) {
             g_cta_trace = nullptr;
@@ -525,7 +532,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           if (g_cta_trace) {
             const int64_t r = g_cta_trace_calls % kTraceCalls;
             if (r == 0) cudaMemsetAsync(g_cta_trace, 0, sizeof(uint64_t) * region * kTraceCalls, st);
-            g_cta_trace_n = 4 * g->sm_count;
+            g_cta_trace_n = 4 * grid;
             fp.trace = g_cta_trace + r * region;
             ++g_cta_trace_calls;
           }
@@ -563,7 +570,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         g_trace.used = 0;
         if (tr) cudaEventRecord(trace_event(0), st);
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)g->sm_count);
+        cfg.gridDim = dim3((unsigned)grid);
         cfg.blockDim = dim3((unsigned)threads);
         cfg.dynamicSmemBytes = smemf;
         cfg.stream = st;

@@ -128,7 +128,8 @@ struct Transposer {
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      const uint32_t y = __shfl_xor_sync(FULL, x, 16 >> k);
+      uint32_t y;                                                   // (inline: no divergence check)
+      asm volatile("shfl.sync.bfly.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(y) : "r"(x), "r"(16 >> k));
       const uint32_t t = __funnelshift_l(y, y, sh[k]);
       // x = (x & K) | (t & ~K) as ONE lop3 (left to itself ptxas splits it into three)
       asm("lop3.b32 %0, %0, %1, %2, 0xE4;" : "+r"(x) : "r"(t), "r"(K[k]));
@@ -387,18 +388,19 @@ __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t 
     x[2 * k] = __uint_as_float((uint32_t)xp[k]);
     x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
   }
+  // t = 0 (x <= 0 or NaN) must never fire, but its bound 256 t - 1 wraps to "always": those
+  // elements are cleared at the end by [x > +0] (the packed compare against theta = +0)
+  const uint32_t pos = pack_sub(xp, 0ull);
 #pragma unroll
   for (int j = 0; j < NT; ++j) word[j] = 0u;
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
-    uint32_t tw[4], qb[4];
+    uint32_t tw[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int q = 4 * q4 + e;
-      const float xs = x[q] * 16777216.0f;
-      const uint32_t t = xs > 16777216.0f ? 16777216u : (uint32_t)ceilf(fmaxf(xs, 0.0f));
-      tw[e] = (t << 8) - 1u;
-      qb[e] = t != 0u ? (1u << q) : 0u;
+      // t = ceil(min(max(x 2^24, 0), 2^24)): fmaxf maps NaN to 0, fminf clamps x > 1 and inf
+      const float xs = fminf(fmaxf(x[4 * q4 + e] * 16777216.0f, 0.0f), 16777216.0f);
+      tw[e] = ((uint32_t)ceilf(xs) << 8) - 1u;                     // 2^24 -> 2^32 - 1: always
     }
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -406,16 +408,19 @@ __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t 
                                     p.key0, p.key1);
       const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) word[j] |= ow[e] <= tw[e] ? qb[e] : 0u;
+      for (int e = 0; e < 4; ++e) word[j] |= ow[e] <= tw[e] ? (1u << (4 * q4 + e)) : 0u;
     }
   }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) word[j] &= pos;
 }
 
 // K1 for the blocked layout (CM_LAYOUT_BLK): the same per-block steps as k1_body, with the
 // bookkeeping hoisted out of the block loop -- a group's row masks, store pointers and table
 // base are set once per group (running pointers inside it), and the producer cursor is a
 // running source pointer whose block sizes follow from (pg, pw) alone.
-template <int NT, bool RAND, class Hooks>
+// MS: the mass tables -- 0 decided at run time (p.nib32 set or not), 1 int32 (staged), 2 int64.
+template <int NT, bool RAND, int MS, class Hooks>
 __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char* k1smem, int wl, int* sq,
                                             const Hooks& hk, int Gr) {
   constexpr int kSt = k1_stages(NT);
@@ -433,7 +438,7 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
     tt[j] = ((uint64_t)b << 32) | b;
   }
   const Transposer transpose(lane);
-  const bool scaled32 = p.nib32 != nullptr;
+  const bool scaled32 = MS == 0 ? p.nib32 != nullptr : MS == 1;
   // every group but the last (h_last rows) is full: 4 KB off-diagonal, 2 304-byte diagonal blocks
   const int h_last = blk_rows(n, Gr - 1);
   const uint32_t off_last = 128u * (uint32_t)h_last, diag_last = 16u * (uint32_t)blk_diag_chunks(h_last);
@@ -606,7 +611,7 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
 // takes queue in `sq` (8 per warp) until the consumer reaches them.
 // RAND: randomized rounding, sample th0 + j instead of threshold th0 + j (one Philox block
 // per four consecutive nodes and sample).
-template <int NT, int LAY, bool RAND, class Hooks>
+template <int NT, int LAY, bool RAND, class Hooks, int MS = 0>
 __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap* tmap, const DiagMaps* dmaps,
                                         unsigned char* k1smem,
                                         int wl, int* sq, const Hooks& hk) {
@@ -627,7 +632,7 @@ __device__ __forceinline__ void k1_body(const RoundParams& p, const CUtensorMap*
     return;
   }
   if constexpr (BLK) {
-    k1_body_blk<NT, RAND>(p, k1smem, wl, sq, hk, Gr);
+    k1_body_blk<NT, RAND, MS>(p, k1smem, wl, sq, hk, Gr);
     return;
   }
   uint64_t tt[NT];                                                  // theta (-0 -> +0) in both halves
@@ -1145,6 +1150,14 @@ __device__ void emit_mask(const ScanParams& p, const uint32_t* ws, int64_t n_can
 }
 
 // Scratch of one K2 warp: shared-memory views (graph blob, E, spilled A' slots) and TMEM.
+// int32 state: the task's 32 checkpoint masses staged into shared memory by cp.async at the
+// task start (CM_STAGE_MASS=1, 4 KB per scan warp) or read from the ring at the end.
+#ifndef CM_STAGE_MASS
+#define CM_STAGE_MASS 1
+#endif
+constexpr bool kStageMassCfg = CM_STAGE_MASS != 0;
+__host__ __device__ constexpr int scan_e_bytes(bool s32) { return s32 ? 4 * 32 * 32 * (kStageMassCfg ? 2 : 1) : 8 * 32 * 32; }
+
 template <typename ET, bool TM>
 struct ScanCtx {
   const int64_t* M;
@@ -1172,7 +1185,7 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
   x.E = reinterpret_cast<ET*>(wr);
   x.massbuf = reinterpret_cast<ET*>(wr + 32 * 32 * sizeof(ET));           // int32 state only
-  x.A.sm = reinterpret_cast<uint32_t*>(wr + (sizeof(ET) == 4 ? 2 : 1) * 32 * 32 * sizeof(ET));   // [slot][lane] (spill part)
+  x.A.sm = reinterpret_cast<uint32_t*>(wr + scan_e_bytes(sizeof(ET) == 4));   // [slot][lane] (spill part)
   x.A.lane = lane;
   x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
   // TMEM: a warp reaches lane quarter (CTA warp index % 4); K2 warp wk takes columns 256 (wk / 4) ..
@@ -1226,7 +1239,7 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   // the group's 32 checkpoint masses (Eq. 6 sums, rows 32g ..; ET-wide: 128 or 256 bytes)
   // -> shared memory [chunk j][lane][16 bytes], asynchronously
   constexpr int kMassChunks = 2 * (int)sizeof(ET);
-  constexpr bool kStageMass = sizeof(ET) == 4;                      // int64: read at the end (smem)
+  constexpr bool kStageMass = kStageMassCfg && sizeof(ET) == 4;     // else read at the end (.cg)
   if (kStageMass && live) {
     const char* msrc = reinterpret_cast<const char*>(cw + block_words(G)) + 32 * sizeof(ET) * (size_t)g;
     const uint32_t mdst = smem_u32(x.massbuf) + 16u * (uint32_t)lane;
@@ -1312,6 +1325,21 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
       for (int e = 0; e < kPer; ++e) {
         const int b = kPer * j + e, r = 32 * g + b;
         if (r < n) pk = max(pk, (r ? (int64_t)mv[e] : 0) + (int64_t)E[32 * b + lane]);
+      }
+    }
+  } else if (sizeof(ET) == 4) {
+    // the group's 32 int32 masses (rows 32g .., 128 bytes, L2-prefetched with the task)
+    const uint4* m4 = reinterpret_cast<const uint4*>(cw + block_words(G)) + 8 * g;
+    uint4 mv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mv[j] = live ? __ldcg(m4 + j) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w4[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int b = 4 * j + e, r = 32 * g + b;
+        if (r < n) pk = max(pk, (r ? (int64_t)(int32_t)w4[e] : 0) + (int64_t)E[32 * b + lane]);
       }
     }
   } else {
@@ -1584,7 +1612,8 @@ struct K1Ring {
 // setmaxnreg to rebalance registers needs whole warpgroups (10 scan warps hang), and 12 do
 // not fit in shared memory at n = 353.
 constexpr int kFusedScanWarps = CM_KF2;
-constexpr int kFusedTmemCols = 512 / ((kFusedScanWarps + 3) / 4);  // per scan warp
+constexpr int kFusedTmem = 512;                                     // TMEM columns per CTA (one per SM)
+constexpr int kFusedTmemCols = kFusedTmem / ((kFusedScanWarps + 3) / 4);  // per scan warp
 __host__ __device__ constexpr int fused_warps(int nt) { return k1_warps(nt) + kFusedScanWarps; }
 // dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
 __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, bool bulk) {
@@ -1638,8 +1667,8 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   for (int i = threadIdx.x; i < sp.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(k2smem)[i] = sp.blob[i];
   if (warp == kFirstScanWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_base)) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_base)), "n"(kFusedTmem) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1655,7 +1684,8 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
     __shared__ int sq[KF1][8];
     const int w1 = kK1High ? warp - kFusedScanWarps : warp;
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
-    k1_body<NT, LAY, RAND>(fp.rp, &tmap, &dmaps, k1smem, w1, sq[w1], hk);
+    // the int32 scan state <=> the int32 mass tables (both: every row mass fits, cm_api.cu)
+    k1_body<NT, LAY, RAND, K1Ring, sizeof(ET) == 4 ? 1 : 2>(fp.rp, &tmap, &dmaps, k1smem, w1, sq[w1], hk);
     if (fp.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(fp.trace + 4 * blockIdx.x + 1), globaltimer());
     fused_exit(fp);
     return;
@@ -1780,7 +1810,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const Fu
   asm volatile("bar.sync 1, %0;" :: "r"(32 * kFusedScanWarps) : "memory");   // the scan warps only
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == kFirstScanWarp)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem_base) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "n"(kFusedTmem) : "memory");
   fused_exit(fp);
 }
 

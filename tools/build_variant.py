@@ -13,3 +13,5 @@ name, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(ROOT, "tune", name + ".so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
 print(B.build(force=True, extra=defs, out_override=out))
+import shutil  # noqa: E402
+shutil.rmtree(os.path.join(os.path.dirname(out), "build"), ignore_errors=True)   # objects: not pushed to the GPU box
