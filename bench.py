@@ -5,8 +5,9 @@ A step = one pass of the whole hot path (a1-a7 of SURVEY §8(a), plus the a8 MIN
 of the keys at N>1) over one batch of synthetic, device-resident S*.
 Default workload: the ResNet-50-shaped training DAG (n=353, |E|=560), G1 LP-like S*,
 theta = 0.5, 16 budgets, 125,000 S* per GPU per step (the 10^6-candidate config sharded
-over 8 GPUs; weak scaling).  Inputs (67.8 GB per GPU in the dense layout with 128-byte
-rows, ld = 384) exceed L2 (126 MB), so no flush is needed between steps.
+over 8 GPUs; weak scaling).  Default S* layout: blocked strict lower triangle (CM_LAYOUT_BLK,
+250.6 KB per S*, 0.85 % over the triangle: 31.3 GB per GPU; --layout dense: 128-byte rows,
+67.8 GB), far above L2 (126 MB), so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
@@ -63,7 +64,7 @@ def parse():
     ap.add_argument("--samples", type=int, default=None,
                     help="randomized rounding (DESIGN.md R1) with this many samples per S* instead of the thresholds")
     ap.add_argument("--batch", type=int, default=None, help="S* per GPU per step")
-    ap.add_argument("--layout", default="dense", choices=["tri4", "dense", "blk"])
+    ap.add_argument("--layout", default="blk", choices=["tri4", "dense", "blk"])
     ap.add_argument("--ld", type=int, default=None,
                     help="dense row stride in floats (default: n rounded up to 32, i.e. 128-byte rows)")
     ap.add_argument("--overlap", default="on", choices=["on", "off"],
@@ -125,15 +126,16 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(cfg, batch):
-    """DRAM bytes (read + write) of one step, from the committed ncu --set full capture
-    (profiles/traffic.json: bytes per S* of K1+K2+K3 for a config), scaled to the batch."""
+def load_traffic(cfg, layout, batch):
+    """DRAM bytes (read + write) of one launch, from the committed ncu --set full capture
+    (profiles/traffic.json[cfg]["layouts"][layout]: bytes per S* of the fused kernel, written by
+    tools/traffic_from_ncu.py), scaled to the batch; None when that layout was not captured."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p)).get(cfg)
+        d = json.load(open(p)).get(cfg, {}).get("layouts", {}).get(layout)
         if d:
-            return d["dram_bytes_per_sstar"] * batch
-    return None
+            return d["dram_bytes_per_sstar"] * batch, d["source"]
+    return None, None
 
 
 class ClockSampler:
@@ -505,7 +507,7 @@ def main():
     path_ms = kern_ms                     # per-call device time (events around each launch, or the
                                           # per-step time when consecutive calls overlap)
     achieved = alg_bytes / (path_ms / 1000.0) / 1e9
-    traffic = load_traffic(a.config, batch)
+    traffic, traffic_src = load_traffic(a.config, a.layout, batch)
     # ---- integer-pipe term (K-mu): measured INT peak, Ops_alg from the oracle's A8 counters ----
     ipk = None
     try:
@@ -541,8 +543,8 @@ def main():
             "unit": int_term["unit"] if binds == "int" else "GB/s",
             "frac": int_term["frac"] if binds == "int" else achieved / peak_gbs,
             "traffic": traffic,
-            "traffic_source": "ncu --set full capture committed under profiles/ (profiles/traffic.json, DRAM "
-                              "bytes read + write per S* x batch); not measured in this run",
+            "traffic_source": ("profiles/traffic.json (DRAM bytes read + write per S* x batch; " + traffic_src +
+                               "); not measured in this run") if traffic_src else "no capture of this layout",
             "terms": {"hbm": hbm_term, "int": int_term},
             "binds": binds,
             "kernel": "cm2::fused_kernel: the whole a1-a7 path in one launch per step (" +

@@ -831,6 +831,27 @@ __global__ void __maxnreg__(NT == 1 ? CM_K1_REGS1 : 128) round_tma_kernel(const 
 // i+1 to step i.  Nodes with a non-adjacent user get a slot (host-assigned, nrec.w), slots
 // < 256 in Tensor Memory, the rest in shared memory.  Per warp in shared memory: E[stage][lane]
 // and the spilled slots [slot][lane].
+// int32 state: the task's 32 checkpoint masses staged into shared memory by cp.async at the
+// task start (CM_STAGE_MASS=1, 4 KB per scan warp) or read from the ring at the end (default:
+// measured within 1 %, and the 32 KB per CTA pay for the Sn rings).
+#ifndef CM_STAGE_MASS
+#define CM_STAGE_MASS 0
+#endif
+constexpr bool kStageMassCfg = CM_STAGE_MASS != 0;
+// The walk's Sn words come through a per-warp shared-memory ring of CM_SN_RING quads (16 bytes
+// per lane each, cp.async.cg, CM_SN_RING - 1 quads = 4 (CM_SN_RING - 1) nodes ahead); 0: the
+// quads ride in registers two quads ahead.
+#ifndef CM_SN_RING
+#define CM_SN_RING 8
+#endif
+// The int64 state keeps the registers (its 8 KB E per warp leaves no room for rings at n ~ 560).
+constexpr int kSnRing = CM_SN_RING;
+static_assert(kSnRing == 0 || (kSnRing >= 2 && (kSnRing & (kSnRing - 1)) == 0), "ring of a power of two quads");
+__host__ __device__ constexpr int sn_ring_quads(bool s32) { return s32 ? kSnRing : 0; }
+__host__ __device__ constexpr int scan_e_bytes(bool s32) {
+  return (s32 ? 4 * 32 * 32 * (kStageMassCfg ? 2 : 1) : 8 * 32 * 32) + 512 * sn_ring_quads(s32);
+}
+
 struct ScanParams {
   const uint4* blob;          // M[n] int64, C[n] int64, pred_ptr, pred_idx, nrec, drec
   int32_t blob_bytes;
@@ -1037,6 +1058,24 @@ __device__ __forceinline__ void node_step(uint32_t Rk, uint32_t diag, uint32_t s
   events<4, ET>(Rk & ~diag, sf, Mk, f, m, E, lane);
 }
 
+// Sn ring of Q quads: quad q of the group's Sn column (nodes 4q .. 4q+3, 16 bytes per lane)
+// lives in slot q mod Q; one cp.async group per quad, issued Q - 1 quads ahead,
+// zero-filled for quads below 0 or candidates / groups without Sn.
+template <int Q>
+__device__ __forceinline__ void sn_fetch(uint32_t snr, const uint4* sn4, int q, bool lsn) {
+  const bool v = lsn && q >= 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;"
+               :: "r"(snr + ((uint32_t)(q & (Q - 1)) << 9)), "l"(sn4 + (v ? q : 0)), "r"(v ? 16 : 0)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
 // Walk the nodes k = nk-1 .. 0 of a group pass, one node per iteration.
 // nrec[k] = {(int32) M_k, e0, ndf | adj << 16, slot_k or -1}.
 template <typename ET, bool TM, int MODE, bool RSTORE>
@@ -1044,12 +1083,27 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
                                      const uint32_t* brow, const int4* __restrict__ nrec,
                                      const int2* __restrict__ drec, const int64_t* __restrict__ M,
                                      const int64_t* __restrict__ C, const AView<TM>& A, ET* E, int lane,
-                                     int64_t& costL) {
+                                     int64_t& costL, uint32_t snr) {
   const int k0 = nk - 1;
-  // Sn words of the quad holding k and of the quad below (for Sn_{k-1}), loaded a quad ahead
-  uint4 quad = lsn ? __ldcg(sn4 + (k0 >> 2)) : make_uint4(0u, 0u, 0u, 0u);
-  uint4 nquad = (lsn && (k0 >> 2) > 0) ? __ldcg(sn4 + (k0 >> 2) - 1) : make_uint4(0u, 0u, 0u, 0u);
-  uint4 n2quad = (lsn && (k0 >> 2) > 1) ? __ldcg(sn4 + (k0 >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
+  constexpr int kQ = sn_ring_quads(sizeof(ET) == 4);
+  constexpr bool kRing = kQ > 0;
+  // registers (no ring): Sn words of the quad holding k and of the two quads below, loaded two
+  // quads ahead.  Ring: quads k0/4 .. k0/4 - kQ + 1 in flight, sp = the address of Sn_{k-1}.
+  uint4 quad = make_uint4(0u, 0u, 0u, 0u), nquad = quad, n2quad = quad;
+  uint32_t sp = 0u;
+  uint32_t sn1;
+  if constexpr (kRing) {
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) sn_fetch<kQ>(snr, sn4, (k0 >> 2) - i, lsn);
+    cp_async_wait<kQ - 1>();
+    sp = snr + ((uint32_t)((k0 >> 2) & (kQ - 1)) << 9) + 4u * (uint32_t)(k0 & 3);
+    sn1 = lds_u32(sp);                                              // Sn_k0
+  } else {
+    quad = lsn ? __ldcg(sn4 + (k0 >> 2)) : make_uint4(0u, 0u, 0u, 0u);
+    nquad = (lsn && (k0 >> 2) > 0) ? __ldcg(sn4 + (k0 >> 2) - 1) : make_uint4(0u, 0u, 0u, 0u);
+    n2quad = (lsn && (k0 >> 2) > 1) ? __ldcg(sn4 + (k0 >> 2) - 2) : make_uint4(0u, 0u, 0u, 0u);
+    sn1 = (k0 & 3) == 3 ? quad.w : (k0 & 3) == 2 ? quad.z : (k0 & 3) == 1 ? quad.y : quad.x;
+  }
   // row 32g's word for k's 32-node block (blocks w < g only; nodes >= 32g are never in S_32g)
   // and, prefetched, for the block below
   const uint32_t bword = (g > 0 && (k0 >> 5) < g && live) ? __ldcg(brow + (k0 >> 5)) : 0u;
@@ -1057,8 +1111,7 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
   uint32_t bcur = bword << (31 - (k0 & 31));                        // bit 31 = node k's bit of row 32g
   uint32_t dg = 1u << (k0 - 32 * g);                                // e_t for k in 32g .. k0 (k0 >= 32g)
   int4 rec1 = nrec[k0];                                             // record of the next node
-  // Sn_k: the previous step's Sn_{k-1}, so each step extracts one word of the quads
-  uint32_t sn1 = (k0 & 3) == 3 ? quad.w : (k0 & 3) == 2 ? quad.z : (k0 & 3) == 1 ? quad.y : quad.x;
+  // Sn_k: the previous step's Sn_{k-1}, so each step extracts one word
   uint32_t acc = 0u;                                                // Acc_k from user k+1
   uint32_t bslot = 0u;                                              // A'_k base when k has a slot
   bool st_pending = true;                                           // init stores precede
@@ -1075,7 +1128,18 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
     rec1 = nrec[k - 1];                                             // k = 0: the sentinel record
     const int64_t Ck = C[k];
     const uint32_t sn = sn1;
-    {  // Sn_{k-1}: component u-1 of the quad, or the next quad's last word (branch-free selects)
+    if constexpr (kRing) {                                          // Sn_{k-1} from the ring
+      if (u == 0) {
+        // quad k/4 - 1 must have landed; slot k/4 is consumed: refill it kQ quads below
+        cp_async_wait<kQ - 2>();
+        sp = snr + ((uint32_t)(((k >> 2) - 1) & (kQ - 1)) << 9) + 12u;
+        sn1 = lds_u32(sp);
+        sn_fetch<kQ>(snr, sn4, (k >> 2) - kQ, lsn);
+      } else {
+        sp -= 4u;
+        sn1 = lds_u32(sp);
+      }
+    } else {  // Sn_{k-1}: component u-1 of the quad, or the next quad's last word (branch-free selects)
       const uint32_t c01 = (u & 2) ? quad.y : quad.x;              // u = 2 -> y, u = 1 -> x
       const uint32_t c = u == 3 ? quad.z : c01;
       sn1 = u == 0 ? nquad.w : c;
@@ -1109,7 +1173,7 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
       A.wait_ld(b1);
     }
     bslot = b1;
-    if (u == 0) {                                                   // next node is in the quad below
+    if (!kRing && u == 0) {                                         // next node is in the quad below
       quad = nquad;                                                 // loads run two quads ahead
       nquad = n2quad;
       n2quad = (lsn && (k >> 2) >= 3) ? __ldcg(sn4 + (k >> 2) - 3) : make_uint4(0u, 0u, 0u, 0u);
@@ -1119,6 +1183,7 @@ __device__ __forceinline__ void walk(int nk, int g, bool live, bool lsn, const u
       bnext = (g > 0 && (k >> 5) >= 2 && live) ? __ldcg(brow + (k >> 5) - 2) : 0u;
     }
   }
+  if constexpr (kRing) cp_async_wait<0>();                          // the next task reuses the slots
 }
 
 // Write one 32x32 mask block set (rows 32g..32g+31 of the 32 candidates of the task) from
@@ -1150,14 +1215,6 @@ __device__ void emit_mask(const ScanParams& p, const uint32_t* ws, int64_t n_can
 }
 
 // Scratch of one K2 warp: shared-memory views (graph blob, E, spilled A' slots) and TMEM.
-// int32 state: the task's 32 checkpoint masses staged into shared memory by cp.async at the
-// task start (CM_STAGE_MASS=1, 4 KB per scan warp) or read from the ring at the end.
-#ifndef CM_STAGE_MASS
-#define CM_STAGE_MASS 1
-#endif
-constexpr bool kStageMassCfg = CM_STAGE_MASS != 0;
-__host__ __device__ constexpr int scan_e_bytes(bool s32) { return s32 ? 4 * 32 * 32 * (kStageMassCfg ? 2 : 1) : 8 * 32 * 32; }
-
 template <typename ET, bool TM>
 struct ScanCtx {
   const int64_t* M;
@@ -1167,6 +1224,7 @@ struct ScanCtx {
   const int32_t* qinfo;
   ET* E;                      // [32 stages][32 lanes]
   ET* massbuf;                // [chunk][32 lanes][16 bytes]: the task's checkpoint masses (rows 32g ..)
+  uint32_t snr;               // shared address of this lane's 16 bytes in quad slot 0 of the Sn ring
   AView<TM> A;
   bool all_tm;
 };
@@ -1185,6 +1243,7 @@ __device__ __forceinline__ ScanCtx<ET, TM> scan_ctx(const ScanParams& p, unsigne
   unsigned char* wr = smem + p.blob_bytes + (size_t)wk * p.warp_bytes;
   x.E = reinterpret_cast<ET*>(wr);
   x.massbuf = reinterpret_cast<ET*>(wr + 32 * 32 * sizeof(ET));           // int32 state only
+  x.snr = smem_u32(wr + scan_e_bytes(sizeof(ET) == 4) - 512 * sn_ring_quads(sizeof(ET) == 4)) + 16u * (uint32_t)lane;
   x.A.sm = reinterpret_cast<uint32_t*>(wr + scan_e_bytes(sizeof(ET) == 4));   // [slot][lane] (spill part)
   x.A.lane = lane;
   x.A.tmc = TM ? min(p.n_slot, tcols) : 0;
@@ -1301,13 +1360,13 @@ __device__ __forceinline__ void scan_task(const ScanParams& p, const ScanCtx<ET,
   int64_t costL = 0;
   uint32_t* rcol = cw + grp_off(g);
   if (p.r_mask32) {
-    if (!TM) walk<ET, TM, 0, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    else if (all_tm) walk<ET, TM, 2, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    else walk<ET, TM, 1, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    if (!TM) walk<ET, TM, 0, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
+    else if (all_tm) walk<ET, TM, 2, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
+    else walk<ET, TM, 1, true>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
   } else {
-    if (!TM) walk<ET, TM, 0, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    else if (all_tm) walk<ET, TM, 2, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
-    else walk<ET, TM, 1, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL);
+    if (!TM) walk<ET, TM, 0, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
+    else if (all_tm) walk<ET, TM, 2, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
+    else walk<ET, TM, 1, false>(nk, g, live, lsn, sn4, rcol, brow, nrec, drec, M, C, A, E, lane, costL, x.snr);
   }
   A.wait_st();                                                    // next task re-fills the slots
   // ---- group result: max_t (mass_t + E_t) over this group's stages, cost sum ----
