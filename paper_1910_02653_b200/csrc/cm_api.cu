@@ -929,6 +929,9 @@ cm_status cm_graph_create(int32_t n, const int32_t* pred_ptr, const int32_t* pre
     if (const char* env = std::getenv("CM_WS_MB")) want = std::max<int64_t>(1, std::atoll(env)) << 20;   // tuning
     g->ws_bytes = std::max<int64_t>(per * 1024, (want / (64 * per)) * 64 * per);
     e = cudaMalloc(&g->d_ws, g->ws_bytes);
+    // zeroed once: a candidate block's words that no kernel writes (the masses of rows >= n and
+    // of row 0, read 16 bytes at a time and discarded) are then defined memory (initcheck-clean)
+    if (e == cudaSuccess) e = cudaMemset(g->d_ws, 0, g->ws_bytes);
   }
   if (e == cudaSuccess) e = cudaMalloc(&g->d_seq, 256);
   if (e == cudaSuccess) e = cudaMemset(g->d_seq, 0, 256);

@@ -1582,13 +1582,14 @@ __device__ __forceinline__ void fused_exit(const FusedParams& fp) {
   // when shared memory allows two CTAs per SM, so residency alone does not order them.
   // Thread 0 (rounding warp 0) gets here when its production ends, well before the tail.
   if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
+  // (non-.aligned barrier: the rounding and the scan warps reach it from different code)
+  asm volatile("barrier.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
   const int64_t words = fused_ctl_words(fp.n_slots);
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(fp.ctl + 2 + 3 * (int64_t)fp.n_slots, 1u) == gridDim.x - 1;
   }
-  asm volatile("bar.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
+  asm volatile("barrier.sync 2, %0;" :: "r"((int)blockDim.x) : "memory");
   if (last && threadIdx.x == 0 && fp.seq_word) {
     // every CTA fenced its outputs before its exit count, and this CTA saw all the counts:
     // publish the call's number to a stream wait on another stream (system-scope release)

@@ -2,6 +2,8 @@
 start while the previous one drains (programmatic dependent launch, alternating workspace
 halves whose control words the kernel clears on exit) and initialises its own keys.  Every
 call's outputs must equal the oracle's, whatever ran before it on the stream."""
+import os
+
 import numpy as np
 import pytest
 
@@ -219,6 +221,8 @@ def test_overlap_randomized_and_max_batch():
 
 
 @pytest.mark.timeout(600)
+@pytest.mark.skipif(os.environ.get("CM_UNDER_SANITIZER") == "1",
+                    reason="compute-sanitizer serialises kernels: no overlap to observe")
 def test_overlap_is_concurrent(env_var):
     """consecutive overlapped calls really run concurrently.  Four bench-size calls
     (ResNet-50, 125 000 S*) with every output allocated before the first one (nothing enqueued
