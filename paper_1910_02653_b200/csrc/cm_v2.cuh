@@ -1437,6 +1437,10 @@ template <typename ET, bool TM>
 __global__ void __launch_bounds__(256, 2) scan_kernel(const ScanParams p) {   // <= 128 regs: co-resides with K1
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
+#ifdef CM_EXP_SCAN_PAD
+  __shared__ uint32_t pad[8];                                       // diagnostic: moves tmem_base
+  if (threadIdx.x < 8) pad[threadIdx.x] = 0u;
+#endif
   __shared__ uint32_t tmem_base;
   for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.blob[i];
@@ -1622,12 +1626,18 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 // lane 0 waits until *p >= target (then the warp proceeds); exponential back-off sleep.  The
 // counters only grow: poll with relaxed loads (an acquire load invalidates L1 -- CCTL.IVALL --
 // every time) and acquire once when the target is reached.
+// CAP: the back-off ceiling in ns -- a producer waiting for a ring slot waits on the scan (a
+// long wait when the scan binds: its polls would only take issue slots from the scan warps).
+#ifndef CM_SLOT_WAIT_NS
+#define CM_SLOT_WAIT_NS 8192
+#endif
+template <uint32_t CAP = 1024>
 __device__ __forceinline__ void warp_wait_geq(const uint32_t* p, uint32_t target) {
   if ((threadIdx.x & 31) == 0) {
     uint32_t ns = 32;
     while (ld_relaxed(p) < target) {
       __nanosleep(ns);
-      ns = ns < 1024 ? 2 * ns : ns;
+      ns = ns < CAP ? 2 * ns : ns;
     }
     (void)ld_acquire(p);
   }
@@ -1652,7 +1662,7 @@ struct K1Ring {
   __device__ __forceinline__ int next(int s) const { return ((s + 1) & (claim - 1)) ? s + 1 : first(); }
   __device__ __forceinline__ uint32_t* begin(int s) const {
     const int u = s >> 5, slot = u % n_slots, k = u / n_slots;
-    if (k > 0 && (s & (claim - 1)) == 0) warp_wait_geq(ctl + 1 + 2 * n_slots + slot, (uint32_t)k);
+    if (k > 0 && (s & (claim - 1)) == 0) warp_wait_geq<CM_SLOT_WAIT_NS>(ctl + 1 + 2 * n_slots + slot, (uint32_t)k);
     return ring + (int64_t)slot * slot_words + (int64_t)(s & 31) * n_theta * cs;
   }
   __device__ __forceinline__ void end(int s) const {
