@@ -496,7 +496,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, fn, threads, smemf);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy(fused_kernel)");
       if (occf >= 1) {
-        const int grid = g->sm_count;                                 // one CTA per SM (all 512 TMEM columns)
+        // one CTA per SM (all 512 TMEM columns), or as many as fit when a CTA takes fewer columns
+        const int grid = g->sm_count * (cm2::kFusedTmem == 512 ? 1 : std::min(occf, 512 / cm2::kFusedTmem));
         if (env_flag("CM_DEBUG", 0)) {
           cudaFuncAttributes fa = {};
           cudaFuncGetAttributes(&fa, fn);

@@ -1682,7 +1682,10 @@ struct K1Ring {
 // setmaxnreg to rebalance registers needs whole warpgroups (10 scan warps hang), and 12 do
 // not fit in shared memory at n = 353.
 constexpr int kFusedScanWarps = CM_KF2;
-constexpr int kFusedTmem = 512;                                     // TMEM columns per CTA (one per SM)
+#ifndef CM_FUSED_TMEM
+#define CM_FUSED_TMEM 512
+#endif
+constexpr int kFusedTmem = CM_FUSED_TMEM;                           // TMEM columns per CTA (512: one CTA per SM)
 constexpr int kFusedTmemCols = kFusedTmem / ((kFusedScanWarps + 3) / 4);  // per scan warp
 __host__ __device__ constexpr int fused_warps(int nt) { return k1_warps(nt) + kFusedScanWarps; }
 // dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
@@ -1705,7 +1708,10 @@ __host__ __device__ constexpr int fused_k2_regs(int nt) {
 
 // ET: the scan state (int32 when sum M / gcd < 2^31, else int64).
 template <int NT, int LAY, bool RAND, typename ET>
-__global__ void __launch_bounds__(32 * fused_warps(NT), 1) fused_kernel(const FusedParams fp,
+#ifndef CM_FUSED_MINB
+#define CM_FUSED_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * fused_warps(NT), CM_FUSED_MINB) fused_kernel(const FusedParams fp,
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const __grid_constant__ DiagMaps dmaps) {
   constexpr int KF1 = k1_warps(NT);
