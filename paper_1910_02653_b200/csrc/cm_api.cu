@@ -497,7 +497,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
       if (e != cudaSuccess) return cuda_fail(e, "occupancy(fused_kernel)");
       if (occf >= 1) {
         // one CTA per SM (all 512 TMEM columns), or as many as fit when a CTA takes fewer columns
-        const int grid = g->sm_count * (cm2::kFusedTmem == 512 ? 1 : std::min(occf, 512 / cm2::kFusedTmem));
+        int per_sm = cm2::kFusedTmem == 512 ? 1 : std::min(occf, 512 / cm2::kFusedTmem);
+        if (cm2::kFusedTmem < 512) per_sm = std::max(1, std::min(512 / cm2::kFusedTmem, env_flag("CM_FUSED_PER_SM", per_sm)));
+        const int grid = g->sm_count * per_sm;
         if (env_flag("CM_DEBUG", 0)) {
           cudaFuncAttributes fa = {};
           cudaFuncGetAttributes(&fa, fn);

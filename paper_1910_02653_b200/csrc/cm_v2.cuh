@@ -388,11 +388,26 @@ __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t 
     x[2 * k] = __uint_as_float((uint32_t)xp[k]);
     x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
   }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) word[j] = 0u;
+  if constexpr (NT == 1) {
+    // one sample: compare in fp32 directly -- k = w >> 8 < 2^24 converts exactly, x 2^24 is
+    // exact (a power-of-two scale; NaN stays NaN: never, x > 1 and inf: always), and
+    // k 2^-24 < x  <=>  k < x 2^24 (I2F + FSETP per element, no bound to build)
+#pragma unroll
+    for (int q4 = 0; q4 < 8; ++q4) {
+      const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)p.th0),
+                                    p.key0, p.key1);
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        word[0] |= (float)(ow[e] >> 8) < x[4 * q4 + e] * 16777216.0f ? (1u << (4 * q4 + e)) : 0u;
+    }
+    return;
+  }
   // t = 0 (x <= 0 or NaN) must never fire, but its bound 256 t - 1 wraps to "always": those
   // elements are cleared at the end by [x > +0] (the packed compare against theta = +0)
   const uint32_t pos = pack_sub(xp, 0ull);
-#pragma unroll
-  for (int j = 0; j < NT; ++j) word[j] = 0u;
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
     uint32_t tw[4];
