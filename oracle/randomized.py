@@ -7,13 +7,15 @@ The paper's randomized rounding of S* draws Pr[S_int = 1] = S*  (Â
 sample many integral solutions"; App. D).  The paper fixes no
 random number generator, so DESIGN.md reading R1 fixes one, exactly reproducible on both sides:
 
-  u(s, j, t, i) = (Philox4x32-10(ctr, key)[(i - 1) mod 4] >> 8) * 2^-24    (24-bit, in [0, 1))
+  u(s, j, t, i) = Philox4x32-10(ctr, key)[(i - 1) mod 4] * 2^-32            (32-bit, in [0, 1))
       ctr = ((i - 1) div 4, t - 1, s mod 2^32, j),  key = (seed mod 2^32, seed div 2^32)
-  S_{t,i} = 1[u(s, j, t, i) < S*_{t,i}]  for i < t                             (fp32 compare)
+  S_{t,i} = 1[u(s, j, t, i) < S*_{t,i}]  for i < t        (exact compare of the real values)
 
 for S* number s (global index) and sample j: one Philox block gives four consecutive nodes of
 one row of one sample (round 2's reading; round 1 took the four samples of one element from a
-block, which wasted three of its words below four samples).  S* = 0 never sets a bit, S* = 1 always does;
+block, which wasted three of its words below four samples).  The uniform is the whole 32-bit
+word (round 2's second reading; the first used its top 24 bits, (w >> 8) 2^-24): u and the
+fp32 S* are both exact in float64, so the compare below is the exact one.  S* = 0 never sets a bit, S* = 1 always does;
 NaN compares false.  Phase 2 (R, FREE, U, cost) is unchanged (checkmate_oracle).
 
 Philox4x32-10 is Salmon et al., "Parallel random numbers: as easy as 1, 2, 3" (SC'11):
@@ -61,19 +63,19 @@ def philox4x32_10_np(c0, c1, c2, c3, k0, k1):
     return [c.astype(np.uint32) for c in (c0, c1, c2, c3)]
 
 
-def uniform24(word):
-    """(word >> 8) * 2^-24 as fp32: exact (a 24-bit integer times a power of two)."""
-    return (np.asarray(word, np.uint32) >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+def uniform32(word):
+    """word * 2^-32 as float64: exact (a 32-bit integer times a power of two)."""
+    return np.asarray(word, np.uint32).astype(np.float64) * 2.0 ** -32
 
 
 def uniforms(n: int, s: int, j: int, seed: int) -> np.ndarray:
-    """u(s, j, t, i) for t, i = 1..n as U[t-1][i-1] (float32); the whole matrix, i < t used."""
+    """u(s, j, t, i) for t, i = 1..n as U[t-1][i-1] (float64); the whole matrix, i < t used."""
     t = np.repeat(np.arange(n, dtype=np.uint64), n)           # t - 1
     i = np.tile(np.arange(n, dtype=np.uint64), n)             # i - 1
     out = philox4x32_10_np(i // np.uint64(4), t, np.full(n * n, s & MASK, np.uint64),
                            np.full(n * n, j & MASK, np.uint64), seed & MASK, (seed >> 32) & MASK)
     word = np.choose((i % np.uint64(4)).astype(np.int64), out)  # output word (i - 1) mod 4
-    return uniform24(word).reshape(n, n)
+    return uniform32(word).reshape(n, n)
 
 
 def round_S_randomized(inst: Instance, sstar, s: int, j: int, seed: int) -> np.ndarray:
@@ -82,7 +84,7 @@ def round_S_randomized(inst: Instance, sstar, s: int, j: int, seed: int) -> np.n
     U = uniforms(n, s, j, seed)
     S = np.zeros((n + 2, n + 1), dtype=bool)
     for t in range(1, n + 1):
-        row = np.asarray(sstar[t - 1][: t - 1], dtype=np.float32)
+        row = np.asarray(sstar[t - 1][: t - 1], dtype=np.float32).astype(np.float64)   # exact
         S[t, 1:t] = U[t - 1, : t - 1] < row      # NaN compares false
     return S
 

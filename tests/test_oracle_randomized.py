@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 from oracle import Instance, evaluate, evaluate_randomized, philox4x32_10, round_S, round_S_randomized, uniforms
-from oracle.randomized import philox4x32_10_np, uniform24
+from oracle.randomized import philox4x32_10_np, uniform32
 from workloads import graphs as G
 from workloads.sstar import from_binary, gen_sstar
 
@@ -28,10 +28,34 @@ def test_philox_known_answers():
 
 
 def test_uniform_mapping_exact():
-    w = np.array([0, 255, 256, 0xFFFFFFFF, 0x80000000], np.uint32)
-    u = uniform24(w)
-    assert u.dtype == np.float32
-    assert list(u) == [0.0, 0.0, 2.0 ** -24, 1.0 - 2.0 ** -24, 0.5]
+    w = np.array([0, 1, 255, 256, 0xFFFFFFFF, 0x80000000], np.uint32)
+    u = uniform32(w)
+    assert u.dtype == np.float64
+    assert list(u) == [0.0, 2.0 ** -32, 255 * 2.0 ** -32, 2.0 ** -24, 1.0 - 2.0 ** -32, 0.5]
+
+
+def test_compare_is_exact_at_the_boundary():
+    """S = 1[u < S*] on the real values (R1): S* equal to a uniform never fires,
+    one fp32 ulp above it does, whatever the word's low bits; S* = 1 always fires, 0 never."""
+    n = 6
+    inst = Instance(n, [], np.zeros(n, np.int64), np.zeros(n, np.int64), 0)
+    U = uniforms(n, 5, 1, 77)
+    x = np.zeros((n, n), np.float32)
+    for t in range(2, n + 1):
+        for i in range(1, t):
+            u = U[t - 1, i - 1]
+            # the fp32 nearest below / at-or-above u: [u < x] is 0 and 1 respectively
+            lo = np.float32(u)
+            lo = lo if float(lo) <= u else np.nextafter(lo, np.float32(0))
+            hi = lo if float(lo) == u else np.nextafter(lo, np.float32(1))
+            hi = hi if float(hi) > u else np.nextafter(hi, np.float32(1))
+            x[t - 1, i - 1] = hi if (t + i) % 2 else lo
+    S = round_S_randomized(inst, x, 5, 1, 77)
+    for t in range(2, n + 1):
+        for i in range(1, t):
+            assert S[t, i] == bool((t + i) % 2), (t, i)
+    assert round_S_randomized(inst, np.ones((n, n), np.float32), 5, 1, 77)[1:n + 1, 1:].sum() == n * (n - 1) // 2
+    assert not round_S_randomized(inst, np.zeros((n, n), np.float32), 5, 1, 77).any()
 
 
 def test_binary_sstar_equals_deterministic():
@@ -77,10 +101,10 @@ def test_uniforms_layout():
     for t in range(1, 10):
         for i in range(1, 10):
             w = philox4x32_10(((i - 1) // 4, t - 1, 3, 6), (11, 7))[(i - 1) % 4]
-            assert U[t - 1, i - 1] == np.float32((w >> 8) * 2.0 ** -24)
+            assert U[t - 1, i - 1] == w / 2.0 ** 32
     # one block serves four consecutive nodes: nodes 1..4 of a row are its four words
     blk = philox4x32_10((0, 2, 3, 6), (11, 7))
-    assert [U[2, q] for q in range(4)] == [np.float32((w >> 8) * 2.0 ** -24) for w in blk]
+    assert [U[2, q] for q in range(4)] == [w / 2.0 ** 32 for w in blk]
 
 
 def test_appendix_d_deterministic_not_worse():

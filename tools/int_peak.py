@@ -6,7 +6,7 @@ on cuda:0: per instruction class, a full-chip grid of long independent chains; l
 second from CUDA events, and the loaded SM clock the kernel itself saw (%clock64 over
 %globaltimer per CTA, median).
 
-    python tools/int_peak.py [--json out.json]
+    python tools/int_peak.py [--pipes] [--json out.json]
 """
 from __future__ import annotations
 
@@ -18,6 +18,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "tools", "libcm_intpeak.so")
 CLASSES = {0: "lop3", 1: "iadd3", 2: "imad", 3: "lop3+imad", 4: "popc", 5: "flo", 6: "shfl", 7: "fsetp+or"}
+# pipe probes (--pipes): which pipe the randomized-rounding K1 instructions issue to
+PIPES = {8: "imad.wide", 9: "i2fp", 10: "shf.l.w", 11: "ffma2", 12: "imad.hi", 13: "lop3+i2fp",
+         14: "lop3+imad.wide", 15: "lop3+imad.hi", 16: "carry-pack", 17: "lop3+ffma2", 18: "lop3+shf",
+         19: "lop3+carry-pack"}
 
 
 def _lib():
@@ -32,7 +36,7 @@ def _lib():
     return lib
 
 
-def measure(iters: int = 8192, reps: int = 3, device: int = 0) -> dict:
+def measure(iters: int = 8192, reps: int = 3, device: int = 0, pipes: bool = False) -> dict:
     import numpy as np
     import torch
     lib = _lib()
@@ -43,7 +47,7 @@ def measure(iters: int = 8192, reps: int = 3, device: int = 0) -> dict:
     clk = torch.zeros(2 * blocks, dtype=torch.int64, device=dev)
     st = torch.cuda.current_stream(dev)
     out = {}
-    for cls, name in CLASSES.items():
+    for cls, name in (dict(CLASSES, **PIPES) if pipes else CLASSES).items():
         rc = lib.cmip_launch(cls, blocks, 64, 1, sink.data_ptr(), clk.data_ptr(), st.cuda_stream)   # warm-up
         if rc != 0:
             raise RuntimeError(f"int_peak launch failed: cudaError {rc}")
@@ -67,8 +71,8 @@ def measure(iters: int = 8192, reps: int = 3, device: int = 0) -> dict:
 
 
 if __name__ == "__main__":
-    r = measure()
+    r = measure(pipes="--pipes" in sys.argv)
     s = json.dumps(r, indent=1)
-    if len(sys.argv) > 2 and sys.argv[1] == "--json":
-        open(sys.argv[2], "w").write(s + "\n")
+    if "--json" in sys.argv:
+        open(sys.argv[sys.argv.index("--json") + 1], "w").write(s + "\n")
     print(s)
