@@ -1,6 +1,7 @@
 // cm_api.cu -- the C ABI declared in include/cm.h (validation, graph upload, launch).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cstdio>
@@ -690,6 +691,12 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
 
 }  // namespace
 
+// host-side NVTX range over one C-ABI call (no-op unless a profiler injects NVTX)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 const char* cm_status_string(cm_status s) {
@@ -1056,6 +1063,7 @@ int32_t cm_graph_n(const cm_graph* g) { return g ? g->n : -1; }
 int64_t cm_graph_cost_bound(const cm_graph* g) { return g ? g->cost_bound : -1; }
 
 cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_stream stream) {
+  const NvtxRange nvtx("cm_round_and_evaluate");
   if (!g || !a) return fail(CM_EINVAL, "NULL graph or args");
   const int n = g->n;
   if (a->n_sstar < 0 || a->n_theta < 1 || a->n_budget < 0) return fail(CM_EINVAL, "bad counts");

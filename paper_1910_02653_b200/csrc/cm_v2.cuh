@@ -376,58 +376,46 @@ struct DiagMaps {
 // a1 word of one 32 x 32 block (row r = rq of this lane, nodes 32w ..): randomized rounding
 // (R1): sample th0 + j of node i-1 = 32w + q in row rq is word q % 4 of the Philox
 // block with counter (8w + q / 4, rq, global S* index, th0 + j): one block per four
-// consecutive nodes and sample.  u = (w >> 8) 2^-24 < x  <=>  (w >> 8) < t = ceil(x 2^24)
-// (exact in fp32; t clamped to [0, 2^24]: x > 1 or inf always, x <= 0 or NaN never)  <=>
-// w <= 256 t - 1 for t >= 1 (t = 2^24 wraps to 2^32 - 1: always); t = 0: never.
+// consecutive nodes and sample, and S = [w 2^-32 < x] exactly.  With X = x 2^32 (exact: a
+// power-of-two scale; x > 2^96 or inf -> +inf, always; NaN stays NaN, never) and f = rz(w)
+// (cvt.rz: the largest float <= w), [w < X] = [f < X] -- X is a float, so X <= w iff X <= f --
+// and [f < X] = sign(f - X) in fp32: a nonzero difference of floats never rounds to 0, f = X
+// gives +0, NaN the canonical NaN (sign 0).  Per element and sample: one I2FP, half a packed
+// FADD2 (sub.rn.f32x2) and one funnel shift of the sign into the word; X once per element
+// (half a packed FMUL2).  Two chains (elements 0..15 and 16..31) for ILP.
 template <int NT>
 __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t (&xp)[16], int w, int rq, uint32_t sg,
                                            const RoundParams& p) {
-  float x[32];
+  uint64_t X[16];                                                   // x 2^32, elements 2k, 2k+1
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    x[2 * k] = __uint_as_float((uint32_t)xp[k]);
-    x[2 * k + 1] = __uint_as_float((uint32_t)(xp[k] >> 32));
-  }
+  for (int k = 0; k < 16; ++k) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(X[k]) : "l"(xp[k]), "l"(0x4f8000004f800000ull));
 #pragma unroll
-  for (int j = 0; j < NT; ++j) word[j] = 0u;
-  if constexpr (NT == 1) {
-    // one sample: compare in fp32 directly -- k = w >> 8 < 2^24 converts exactly, x 2^24 is
-    // exact (a power-of-two scale; NaN stays NaN: never, x > 1 and inf: always), and
-    // k 2^-24 < x  <=>  k < x 2^24 (I2F + FSETP per element, no bound to build)
+  for (int j = 0; j < NT; ++j) {
+    uint32_t hi = 0u, lo = 0u;
 #pragma unroll
-    for (int q4 = 0; q4 < 8; ++q4) {
-      const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)p.th0),
-                                    p.key0, p.key1);
-      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        word[0] |= (float)(ow[e] >> 8) < x[4 * q4 + e] * 16777216.0f ? (1u << (4 * q4 + e)) : 0u;
+    for (int q4 = 3; q4 >= 0; --q4) {                               // blocks q4 + 4 (hi) and q4 (lo)
+      const uint4 oh = philox4x32_10(make_uint4((uint32_t)(8 * w + q4 + 4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
+                                     p.key0, p.key1);
+      const uint4 ol = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
+                                     p.key0, p.key1);
+      auto pack4 = [&](uint32_t& acc, const uint4& o, int k0) {     // elements 2k0 .. 2k0 + 3, descending
+        uint64_t f23, f01, d23, d01;
+        asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+            : "=l"(f23) : "r"(o.z), "r"(o.w));
+        asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+            : "=l"(f01) : "r"(o.x), "r"(o.y));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(f23), "l"(X[k0 + 1]));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(f01), "l"(X[k0]));
+        acc = __funnelshift_l((uint32_t)(d23 >> 32), acc, 1);       // element 2k0 + 3
+        acc = __funnelshift_l((uint32_t)d23, acc, 1);               // element 2k0 + 2
+        acc = __funnelshift_l((uint32_t)(d01 >> 32), acc, 1);       // element 2k0 + 1
+        acc = __funnelshift_l((uint32_t)d01, acc, 1);               // element 2k0
+      };
+      pack4(hi, oh, 2 * (q4 + 4));
+      pack4(lo, ol, 2 * q4);
     }
-    return;
+    word[j] = (hi << 16) | lo;
   }
-  // t = 0 (x <= 0 or NaN) must never fire, but its bound 256 t - 1 wraps to "always": those
-  // elements are cleared at the end by [x > +0] (the packed compare against theta = +0)
-  const uint32_t pos = pack_sub(xp, 0ull);
-#pragma unroll
-  for (int q4 = 0; q4 < 8; ++q4) {
-    uint32_t tw[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      // t = ceil(min(max(x 2^24, 0), 2^24)): fmaxf maps NaN to 0, fminf clamps x > 1 and inf
-      const float xs = fminf(fmaxf(x[4 * q4 + e] * 16777216.0f, 0.0f), 16777216.0f);
-      tw[e] = ((uint32_t)ceilf(xs) << 8) - 1u;                     // 2^24 -> 2^32 - 1: always
-    }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const uint4 o = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
-                                    p.key0, p.key1);
-      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) word[j] |= ow[e] <= tw[e] ? (1u << (4 * q4 + e)) : 0u;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NT; ++j) word[j] &= pos;
 }
 
 #ifndef CM_BLK_EVICT_FIRST

@@ -16,9 +16,11 @@ def global_best(best_key, group=None):
     """In-place all-reduce MIN of the int64 keys; equal keys cannot come from two ranks
     because the index field is global, so the result is the global (cost, idx) argmin.
     The max-batch keys ((2^31-1 - B_max) << idx_bits | idx) reduce the same way."""
+    import torch
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(best_key, op=dist.ReduceOp.MIN, group=group)
+        with torch.cuda.nvtx.range("cm_allreduce_min"):
+            dist.all_reduce(best_key, op=dist.ReduceOp.MIN, group=group)
     return best_key
 
 
@@ -43,7 +45,8 @@ def gather_winner_masks(best_key, idx_bits: int, index_base: int, r_mask, s_mask
             out[b, 0] = r_mask[local]
             out[b, 1] = s_mask[local]
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+        with torch.cuda.nvtx.range("cm_gather_winner_masks"):
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     return out
 
 

@@ -47,7 +47,7 @@ def measure(iters: int = 8192, reps: int = 3, device: int = 0, pipes: bool = Fal
     clk = torch.zeros(2 * blocks, dtype=torch.int64, device=dev)
     st = torch.cuda.current_stream(dev)
     out = {}
-    for cls, name in (dict(CLASSES, **PIPES) if pipes else CLASSES).items():
+    for cls, name in ({**CLASSES, **PIPES} if pipes else CLASSES).items():
         rc = lib.cmip_launch(cls, blocks, 64, 1, sink.data_ptr(), clk.data_ptr(), st.cuda_stream)   # warm-up
         if rc != 0:
             raise RuntimeError(f"int_peak launch failed: cudaError {rc}")

@@ -62,10 +62,11 @@ class DeviceGenerator:
         count = out.shape[0]
         if stream is None:
             stream = torch.cuda.current_stream(out.device).cuda_stream
-        rc = lib.cmgen_sstar(self.g.n, self.g.L, self.last.data_ptr(), self.lastF.data_ptr(),
-                             self.family, self.seed, int(s_begin), int(count),
-                             {"dense": 0, "tri4": 1, "blk": 2}[self.layout], self.ld, self.stride,
-                             float(upper), float(SIGMA_SCALE), out.data_ptr(), ctypes.c_void_p(stream))
+        with torch.cuda.nvtx.range("cm_generate_sstar"):
+            rc = lib.cmgen_sstar(self.g.n, self.g.L, self.last.data_ptr(), self.lastF.data_ptr(),
+                                 self.family, self.seed, int(s_begin), int(count),
+                                 {"dense": 0, "tri4": 1, "blk": 2}[self.layout], self.ld, self.stride,
+                                 float(upper), float(SIGMA_SCALE), out.data_ptr(), ctypes.c_void_p(stream))
         if rc != 0:
             raise RuntimeError(f"cmgen_sstar failed: cudaError {rc}")
         return out
