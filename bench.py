@@ -520,6 +520,12 @@ def main():
         cpu, counters = cpu_oracle_rate(a.config, fam, seed, thetas, a.cpu_seconds)
     if counters:
         ops_pc, ops_src = ops_alg_of(g.n, counters), f"oracle A8 counters of the cpu_baseline sample ({len(counters)} candidates)"
+    elif a.samples:
+        # the randomized candidates' own phase-2 counters (their S differ from the rounded ones:
+        # about twice the closure, frees and recomputes of G1 at theta 0.5)
+        ops_pc, ops_src = load_ops_alg(a.config, "rand_" + fam)
+        if ops_pc is None:
+            ops_pc, ops_src = load_ops_alg(a.config, fam)
     else:
         ops_pc, ops_src = load_ops_alg(a.config, fam)
     if a.samples:

@@ -382,37 +382,70 @@ struct DiagMaps {
 // and [f < X] = sign(f - X) in fp32: a nonzero difference of floats never rounds to 0, f = X
 // gives +0, NaN the canonical NaN (sign 0).  Per element and sample: one I2FP, half a packed
 // FADD2 (sub.rn.f32x2) and one funnel shift of the sign into the word; X once per element
-// (half a packed FMUL2).  Two chains (elements 0..15 and 16..31) for ILP.
+// (half a packed FMUL2).  Two pack chains (elements 0..15 and 16..31); CM_RAND_ILP Philox
+// blocks in flight.
+#ifndef CM_RAND_ILP
+#define CM_RAND_ILP 2
+#endif
+// KB Philox blocks advanced round by round together (independent chains side by side, so the
+// IMAD.WIDE -> LOP3 latency of one chain is covered by the others)
+template <int KB>
+__device__ __forceinline__ void philox_xk(uint4 (&c)[KB], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0[KB], p1[KB];
+#pragma unroll
+    for (int b = 0; b < KB; ++b) {
+      p0[b] = (uint64_t)0xD2511F53u * c[b].x;
+      p1[b] = (uint64_t)0xCD9E8D57u * c[b].z;
+    }
+#pragma unroll
+    for (int b = 0; b < KB; ++b)
+      c[b] = make_uint4((uint32_t)(p1[b] >> 32) ^ c[b].y ^ k0, (uint32_t)p1[b], (uint32_t)(p0[b] >> 32) ^ c[b].w ^ k1,
+                        (uint32_t)p0[b]);
+  }
+}
 template <int NT>
 __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t (&xp)[16], int w, int rq, uint32_t sg,
                                            const RoundParams& p) {
   uint64_t X[16];                                                   // x 2^32, elements 2k, 2k+1
 #pragma unroll
   for (int k = 0; k < 16; ++k) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(X[k]) : "l"(xp[k]), "l"(0x4f8000004f800000ull));
+  auto pack4 = [&](uint32_t& acc, const uint4& o, int k0) {         // elements 2k0 .. 2k0 + 3, descending
+    uint64_t f23, f01, d23, d01;
+    asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+        : "=l"(f23) : "r"(o.z), "r"(o.w));
+    asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+        : "=l"(f01) : "r"(o.x), "r"(o.y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(f23), "l"(X[k0 + 1]));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(f01), "l"(X[k0]));
+    acc = __funnelshift_l((uint32_t)(d23 >> 32), acc, 1);           // element 2k0 + 3
+    acc = __funnelshift_l((uint32_t)d23, acc, 1);                   // element 2k0 + 2
+    acc = __funnelshift_l((uint32_t)(d01 >> 32), acc, 1);           // element 2k0 + 1
+    acc = __funnelshift_l((uint32_t)d01, acc, 1);                   // element 2k0
+  };
+  constexpr int KH = CM_RAND_ILP / 2;                               // blocks per chain per step
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     uint32_t hi = 0u, lo = 0u;
 #pragma unroll
-    for (int q4 = 3; q4 >= 0; --q4) {                               // blocks q4 + 4 (hi) and q4 (lo)
-      const uint4 oh = philox4x32_10(make_uint4((uint32_t)(8 * w + q4 + 4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
-                                     p.key0, p.key1);
-      const uint4 ol = philox4x32_10(make_uint4((uint32_t)(8 * w + q4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
-                                     p.key0, p.key1);
-      auto pack4 = [&](uint32_t& acc, const uint4& o, int k0) {     // elements 2k0 .. 2k0 + 3, descending
-        uint64_t f23, f01, d23, d01;
-        asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
-            : "=l"(f23) : "r"(o.z), "r"(o.w));
-        asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
-            : "=l"(f01) : "r"(o.x), "r"(o.y));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(f23), "l"(X[k0 + 1]));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(f01), "l"(X[k0]));
-        acc = __funnelshift_l((uint32_t)(d23 >> 32), acc, 1);       // element 2k0 + 3
-        acc = __funnelshift_l((uint32_t)d23, acc, 1);               // element 2k0 + 2
-        acc = __funnelshift_l((uint32_t)(d01 >> 32), acc, 1);       // element 2k0 + 1
-        acc = __funnelshift_l((uint32_t)d01, acc, 1);               // element 2k0
-      };
-      pack4(hi, oh, 2 * (q4 + 4));
-      pack4(lo, ol, 2 * q4);
+    for (int q = 4 - KH; q >= 0; q -= KH) {                         // blocks q .. q+KH-1 (lo), +4 (hi)
+      uint4 o[2 * KH];
+#pragma unroll
+      for (int b = 0; b < KH; ++b) {
+        o[b] = make_uint4((uint32_t)(8 * w + q + b + 4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j));
+        o[KH + b] = make_uint4((uint32_t)(8 * w + q + b), (uint32_t)rq, sg, (uint32_t)(p.th0 + j));
+      }
+      philox_xk<2 * KH>(o, p.key0, p.key1);
+#pragma unroll
+      for (int b = KH - 1; b >= 0; --b) {
+        pack4(hi, o[b], 2 * (q + b + 4));
+        pack4(lo, o[KH + b], 2 * (q + b));
+      }
     }
     word[j] = (hi << 16) | lo;
   }
