@@ -72,6 +72,10 @@ def parse():
                          "alternating output sets (a call starts while the previous one drains)")
     ap.add_argument("--step-events", action="store_true",
                     help="with --overlap on: also record CUDA events around every call")
+    ap.add_argument("--keys", default="nccl", choices=["nccl", "nvls"],
+                    help="a8 at N>1: NCCL MIN all-reduce of each call's keys on a side stream (default), "
+                         "or nvls: multimem.red.min into an NVLink multicast buffer inside the reduce step "
+                         "(dist.MulticastKeys; also runs at N=1 on a one-device multicast object)")
     ap.add_argument("--e2e-batch", type=int, default=16384)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -334,8 +338,25 @@ def main():
     n_calls = max(a.warmup, 3) + a.steps + 8
     # one key vector per call (tiny): call i's keys may still be in the MIN all-reduce on the side
     # stream while calls i+1, i+2 run, so no call reuses another's keys
-    keys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev)
-    bkeys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev) if a.max_batch else None
+    nvls = a.keys == "nvls"
+    mkeys = mbkeys = None
+    if nvls:
+        # a8 inside the kernel: every call has its own slot of a multicast buffer, set to
+        # CM_KEY_NONE once on every rank before any call (no per-call init, no all-reduce)
+        from paper_1910_02653_b200.dist import MulticastKeys
+        mkeys = MulticastKeys(n_calls * len(budgets))
+        keys = mkeys.local.view(n_calls, len(budgets))
+        mkeys.reset()
+        if a.max_batch:
+            mbkeys = MulticastKeys(n_calls * len(budgets))
+            mbkeys.reset()
+        bkeys = mbkeys.local.view(n_calls, len(budgets)) if mbkeys else None
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    else:
+        keys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev)
+        bkeys = torch.empty((n_calls, len(budgets)), dtype=torch.int64, device=dev) if a.max_batch else None
     from workloads.budgets import eq13_cost_limit
     limit = eq13_cost_limit(g) if a.max_batch else None
     peaks = [torch.empty(batch * n_theta, dtype=torch.int64, device=dev) for _ in range(n_sets)]
@@ -354,20 +375,23 @@ def main():
         calls[0] += 1
         h = c % n_sets
         key, bkey = keys[c % n_calls], (bkeys[c % n_calls] if bkeys is not None else None)
-        if not ovl:
+        if not ovl and not nvls:
             key.fill_(cm.CM_KEY_NONE)
             if bkey is not None:
                 bkey.fill_(cm.CM_KEY_NONE)
         if i is not None and events:
             k_start[i].record(stream)
+        slot = 8 * len(budgets) * (c % n_calls)
         cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
                               index_base=s_base * n_theta, total_candidates=total, best_key=key,
                               peak=peaks[h], cost=costs[h], stream=stream.cuda_stream, samples=a.samples,
                               seed=seed, cost_limit=limit, best_batch_key=bkey,
-                              init_keys=ovl, overlap=ovl)
+                              init_keys=ovl and not nvls, overlap=ovl,
+                              best_key_mc=mkeys.mc + slot if nvls else None,
+                              best_batch_key_mc=mbkeys.mc + slot if mbkeys else None)
         if i is not None and events:
             k_end[i].record(stream)
-        if world > 1:
+        if world > 1 and not nvls:
             # a8: MIN all-reduce of this call's keys on the side stream, which waits for the call
             # through the library's device-side completion word -- nothing is enqueued on `stream`
             cm.stream_wait_call(graph, cm.last_call_seq(graph), side.cuda_stream)
@@ -411,12 +435,13 @@ def main():
                else elapsed_ms / a.steps)
     # isolated launch: serial calls (keys filled first, no overlap), CUDA events on `stream`
     iso = []
+    iso_key = torch.empty(len(budgets), dtype=torch.int64, device=dev)
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        keys[0].fill_(cm.CM_KEY_NONE)
+        iso_key.fill_(cm.CM_KEY_NONE)
         e0.record(stream)
         cm.round_and_evaluate(graph, sstar, None if a.samples else th, bu, layout=a.layout,
-                              index_base=s_base * n_theta, total_candidates=total, best_key=keys[0],
+                              index_base=s_base * n_theta, total_candidates=total, best_key=iso_key,
                               peak=peaks[0], cost=costs[0], stream=stream.cuda_stream, samples=a.samples, seed=seed)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -568,11 +593,15 @@ def main():
                                    + (f"randomized rounding, {a.samples} samples per S*" if a.samples
                                       else f"theta={thetas}") + f", {len(budgets)} budgets",
                        "global_batch": cand_per_step, "per_gpu_sstar": batch, "layout": a.layout,
-                       "parallelism": f"candidates sharded over {world} GPU(s) ({backend if world > 1 else 'no'} "
-                                      "MIN all-reduce of each step's keys on a side stream)",
+                       "parallelism": (f"candidates sharded over {world} GPU(s) (a8: multimem.red.min of each "
+                                       "call's keys into an NVLink multicast buffer inside the reduce step)"
+                                       if nvls else
+                                       f"candidates sharded over {world} GPU(s) ({backend if world > 1 else 'no'} "
+                                       "MIN all-reduce of each step's keys on a side stream)"),
                        "l2": f"inputs {batch * gen.stride * 4 / 1e9:.1f} GB per GPU > 126 MB L2; no flush",
-                       "calls": ("overlapped: CM_EVAL_OVERLAP | CM_EVAL_INIT_KEYS, two alternating output "
-                                 "sets" if overlap else "serial: keys filled by the caller before each call")},
+                       "calls": ("overlapped: CM_EVAL_OVERLAP" + ("" if nvls else " | CM_EVAL_INIT_KEYS")
+                                 + ", two alternating output sets" if overlap
+                                 else "serial: keys filled by the caller before each call")},
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks,
             "best": [cm.decode_key(k, cm.key_idx_bits(total)) for k in best]}

@@ -135,6 +135,15 @@ typedef struct {
                                  the call writes none of its inputs and touches none of its outputs
                                  (peak, cost, keys, masks) -- e.g. the previous call of a loop that
                                  alternates two output sets.  Ignored with a caller `workspace`. */
+  int64_t* best_key_mc;     /* NULL, or the NVLink multicast view (cm_mc_bind's mc_ptr) of the
+                               buffer whose local unicast view is best_key: the a8 MIN over ranks
+                                then happens in the reduce step itself -- each key goes
+                               out as multimem.red.min.s64 to best_key_mc[b], which the NVSwitch
+                               applies to every participating GPU's replica (best_key is still read
+                               as a filter).  The caller initialises every replica to CM_KEY_NONE
+                               before any rank's call and synchronises all ranks after their calls
+                               before reading; CM_EVAL_INIT_KEYS is rejected (CM_EINVAL). */
+  int64_t* best_batch_key_mc; /* the same for best_batch_key (NULL: atomics on best_batch_key) */
 } cm_eval_args;
 #define CM_EVAL_INIT_KEYS 1
 #define CM_EVAL_OVERLAP 2
@@ -261,6 +270,31 @@ cm_status cm_policy_checkpoints(int32_t n, int32_t L, const int32_t* pred_ptr, c
 cm_status cm_policy_sstar(const cm_graph* g, int32_t L, int32_t n_sets, const uint8_t* k_sets, float* sstar,
                           int64_t ld, cm_stream stream);
 const char* cm_policy_last_error(void);
+
+/*
+ * NVLink SHARP multicast buffers for the a8 key reduction (the paper has no
+ * distributed path -- a8 serves the per-budget sweep of Fig. 5, at scale).
+ * Host functions; one process per GPU, the calling thread's current device.  Sequence:
+ *   rank 0: cm_mc_create(bytes, n_ranks) -> cm_mc_export_fd -> send the fd to the other ranks
+ *   others: cm_mc_import_fd(fd, cm_mc_size of rank 0's object)
+ *   every rank: cm_mc_add_device; barrier; cm_mc_bind -> (uc_ptr, mc_ptr); barrier
+ * uc_ptr is this GPU's replica (plain device memory), mc_ptr the multicast view: a
+ * multimem.red through mc_ptr updates every rank's replica.  Sizes round up to the multicast
+ * granularity (cm_mc_size).  cm_mc_supported: 1 if the current device reports
+ * CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED.  Errors: CM_EINVAL (arguments / call order),
+ * CM_ECUDA (driver; cm_mc_last_error has the CUresult).  cm_mc_destroy unmaps and releases
+ * (after a device synchronisation).  The object is exportable as a POSIX file descriptor.
+ */
+typedef struct cm_mc cm_mc;
+int32_t cm_mc_supported(void);
+cm_status cm_mc_create(int64_t bytes, int32_t n_devices, cm_mc** out);
+cm_status cm_mc_export_fd(const cm_mc* m, int32_t* fd);
+cm_status cm_mc_import_fd(int32_t fd, int64_t bytes, cm_mc** out);
+int64_t cm_mc_size(const cm_mc* m);
+cm_status cm_mc_add_device(cm_mc* m);
+cm_status cm_mc_bind(cm_mc* m, void** uc_ptr, void** mc_ptr);
+void cm_mc_destroy(cm_mc* m);
+const char* cm_mc_last_error(void);
 
 const char* cm_status_string(cm_status s);
 const char* cm_last_error(void);

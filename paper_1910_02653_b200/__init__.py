@@ -219,7 +219,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
                        index_base: int = 0, total_candidates: int | None = None,
                        best_key=None, masks: bool = False, peak=None, cost=None, stream=None,
                        samples: int | None = None, seed: int = 0, cost_limit: int | None = None,
-                       best_batch_key=None, init_keys: bool = False, overlap: bool = False):
+                       best_batch_key=None, init_keys: bool = False, overlap: bool = False,
+                       best_key_mc: int | None = None, best_batch_key_mc: int | None = None):
     """cm_round_and_evaluate on device tensors.
 
     sstar : float32 CUDA tensor; dense [N_S, n, ld], tri4 [N_S, tri4_size(n)] or blk
@@ -234,6 +235,9 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     overlap: the call may start while the previous kernel on the stream drains
             (CM_EVAL_OVERLAP): only when that work writes none of this call's inputs and touches
             none of its outputs, e.g. consecutive calls alternating two output sets.
+    best_key_mc / best_batch_key_mc: device addresses (ints) of the NVLink multicast views of
+            best_key / best_batch_key (dist.MulticastKeys): the a8 MIN over ranks then happens in
+            the reduce step (multimem.red.min); the caller initialises all replicas first.
     Returns dict(peak, cost, best_key, idx_bits, r_mask, s_mask) of CUDA tensors.
     Asynchronous on ``stream`` (default: torch's current stream).
     """
@@ -301,6 +305,8 @@ def round_and_evaluate(graph: Graph, sstar, theta, budget=None, *, layout: str =
     a.best_key = _ptr(best_key)
     a.r_mask = _ptr(r_mask)
     a.s_mask = _ptr(s_mask)
+    a.best_key_mc = int(best_key_mc) if best_key_mc else None
+    a.best_batch_key_mc = int(best_batch_key_mc) if best_batch_key_mc else None
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream
     _check(_lib.cm_round_and_evaluate(graph.handle, ctypes.byref(a), ctypes.c_void_p(stream)),

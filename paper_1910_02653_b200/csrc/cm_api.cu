@@ -455,6 +455,8 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   qp.best_key = a->best_key;
   qp.best_batch_key = a->best_batch_key;
   qp.cost_limit = a->cost_limit;
+  qp.best_key_mc = a->best_key_mc;
+  qp.best_batch_key_mc = a->best_batch_key_mc;
 
   // ---- fused persistent path (one launch; see cm2::fused_kernel) ----
   if ((g->scan32 || !rnd) && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
@@ -1086,6 +1088,14 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
       return fail(CM_EINVAL, "NULL theta/peak/cost");
   }
   if (a->n_budget > 0 && (!a->budget || !a->best_key)) return fail(CM_EINVAL, "NULL budget/best_key");
+  if (a->best_key_mc || a->best_batch_key_mc) {
+    if (a->flags & CM_EVAL_INIT_KEYS)
+      return fail(CM_EINVAL, "multicast keys: CM_EVAL_INIT_KEYS would race other ranks' reductions");
+    if ((a->best_key_mc && !a->best_key) || (a->best_batch_key_mc && !a->best_batch_key))
+      return fail(CM_EINVAL, "multicast keys need the local (unicast) view too");
+    if ((reinterpret_cast<uintptr_t>(a->best_key_mc) | reinterpret_cast<uintptr_t>(a->best_batch_key_mc)) & 7)
+      return fail(CM_EINVAL, "multicast keys not 8-byte aligned");
+  }
   if (a->best_batch_key && cm_key_idx_bits(a->total_candidates) > 32)
     return fail(CM_ERANGE, "max-batch keys need total_candidates <= 2^32");
   if (a->n_budget > 4096) return fail(CM_ERANGE, "n_budget > 4096");
@@ -1118,9 +1128,9 @@ cm_status cm_round_and_evaluate(const cm_graph* g, const cm_eval_args* a, cm_str
     if (e0 != cudaSuccess) return cuda_fail(e0, "earlier asynchronous error");
     return launch_v2(const_cast<cm_graph*>(g), a, reinterpret_cast<cudaStream_t>(stream), idx_bits);
   }
-  if (a->rounding != CM_ROUND_THRESHOLD || a->best_batch_key || a->layout == CM_LAYOUT_BLK)
-    return fail(CM_ERANGE, "randomized rounding / max-batch / the blocked layout need the stage-sliced kernels "
-                           "(graph too large for them)");
+  if (a->rounding != CM_ROUND_THRESHOLD || a->best_batch_key || a->layout == CM_LAYOUT_BLK || a->best_key_mc)
+    return fail(CM_ERANGE, "randomized rounding / max-batch / the blocked layout / multicast keys need the "
+                           "stage-sliced kernels (graph too large for them)");
 
   const int G = (n + 31) / 32;
   const int tri_words = 16 * G * (G + 1);

@@ -1546,7 +1546,20 @@ struct ReduceParams {
   // key ((2^31-1 - B_max) << idx_bits) | idx, atomicMin into best_batch_key (nullptr: off)
   int64_t cost_limit;
   int64_t* best_batch_key;
+  // a8 in the reduce step: NVLink multicast views of best_key / best_batch_key
+  // (nullptr: atomics on the local buffers).  multimem.red.min reaches every GPU's replica.
+  int64_t* best_key_mc;
+  int64_t* best_batch_key_mc;
 };
+
+// MIN of key into *p: a multicast address (every participating GPU's replica, reduced in the
+// NVSwitch) or the local buffer.  Keys are >= 0, so the signed MIN is the key order.
+__device__ __forceinline__ void key_min(int64_t* local, int64_t* mc, int b, int64_t key) {
+  if (mc)
+    asm volatile("multimem.red.relaxed.sys.global.min.s64 [%0], %1;" :: "l"(mc + b), "l"(key) : "memory");
+  else
+    atomicMin(reinterpret_cast<long long*>(local + b), (long long)key);
+}
 
 // peak / cost / a7 keys of candidate c (part rows c, output index out_base + c).
 __device__ __forceinline__ void reduce_one(const ReduceParams& p, const int64_t* part, int64_t c, int64_t out_base) {
@@ -1564,7 +1577,7 @@ __device__ __forceinline__ void reduce_one(const ReduceParams& p, const int64_t*
   for (int b = 0; b < p.n_budget; ++b) {
     if (pk <= __ldg(p.budget + b)) {
       const int64_t cur = *reinterpret_cast<volatile const int64_t*>(p.best_key + b);
-      if (key < cur) atomicMin(reinterpret_cast<long long*>(p.best_key + b), (long long)key);
+      if (key < cur) key_min(p.best_key, p.best_key_mc, b, key);
     }
   }
   if (p.best_batch_key && cs <= p.cost_limit) {
@@ -1575,7 +1588,7 @@ __device__ __forceinline__ void reduce_one(const ReduceParams& p, const int64_t*
       if (bm >= 1) {
         const int64_t k2 = ((kCap - bm) << p.idx_bits) | (p.index_base + local);
         const int64_t cur = *reinterpret_cast<volatile const int64_t*>(p.best_batch_key + b);
-        if (k2 < cur) atomicMin(reinterpret_cast<long long*>(p.best_batch_key + b), (long long)k2);
+        if (k2 < cur) key_min(p.best_batch_key, p.best_batch_key_mc, b, k2);
       }
     }
   }

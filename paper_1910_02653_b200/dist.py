@@ -59,3 +59,113 @@ def decode_keys(best_key, idx_bits: int):
         else:
             out.append((k >> idx_bits, k & ((1 << idx_bits) - 1) if idx_bits else 0))
     return out
+
+
+# ----------------------------------------------------------------------------- NVLS keys
+# The a8 MIN inside the reduce step: a multicast buffer spans the ranks' GPUs;
+# every call reduces its keys with multimem.red.min into it (cm_eval_args.best_key_mc), and
+# after all ranks' calls (one barrier) every GPU's replica holds the global per-budget keys --
+# no all-reduce per step.
+
+def share_fd(fd, group=None):
+    """Give rank 0's file descriptor to every rank of the group (a duplicate on each rank;
+    rank 0 gets its own fd back).  Over an abstract Unix socket whose name rank 0 broadcasts
+    (SCM_RIGHTS); the process group only carries the name.  Host logic: no GPU involved."""
+    import os
+    import socket
+    import uuid
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world == 1:
+        return fd
+    name = [None]
+    if rank == 0:
+        name[0] = "\0cm_mc_" + uuid.uuid4().hex
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name[0])
+        srv.listen(world)
+    dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    if rank == 0:
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            with conn:
+                socket.send_fds(conn, [b"x"], [fd])
+        srv.close()
+        dist.barrier(group=group)
+        return fd
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect(name[0])
+    with cli:
+        _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+    dist.barrier(group=group)
+    return fds[0] if fds else os.dup(fd)
+
+
+class _CAI:
+    """__cuda_array_interface__ view of raw device memory (no ownership)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+
+class MulticastKeys:
+    """``n_keys`` int64 keys in an NVLink multicast buffer across the group's GPUs (cm_mc_*).
+
+    .local  torch int64 tensor: this GPU's replica (pass as best_key; read after a barrier)
+    .mc     int: the multicast address (pass as best_key_mc)
+    Collective over the group (one process per GPU).  Raises CMError where the device or the
+    driver offers no multicast (cm_mc_supported() == 0)."""
+
+    def __init__(self, n_keys: int, group=None):
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import CMError, _lib
+        P = ctypes.c_void_p
+
+        def _check(status, where):
+            if status != 0:
+                raise CMError(status, where + ": " + _lib.cm_mc_last_error().decode())
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        rank = dist.get_rank(group) if world > 1 else 0
+        self._lib = _lib
+        h = P()
+        nbytes = 8 * int(n_keys)
+        if rank == 0:
+            _check(_lib.cm_mc_create(nbytes, world, ctypes.byref(h)), "cm_mc_create")
+        if world > 1:
+            fd = ctypes.c_int32(-1)
+            size = [int(_lib.cm_mc_size(h)) if rank == 0 else 0]
+            if rank == 0:
+                _check(_lib.cm_mc_export_fd(h, ctypes.byref(fd)), "cm_mc_export_fd")
+            dist.broadcast_object_list(size, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            got = share_fd(fd.value if rank == 0 else -1, group)
+            if rank != 0:
+                _check(_lib.cm_mc_import_fd(got, size[0], ctypes.byref(h)), "cm_mc_import_fd")
+        self.handle = h
+        _check(_lib.cm_mc_add_device(h), "cm_mc_add_device")
+        if world > 1:
+            dist.barrier(group=group)           # every device added before any binds
+        uc, mc = P(), P()
+        _check(_lib.cm_mc_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "cm_mc_bind")
+        if world > 1:
+            dist.barrier(group=group)
+        self.mc = int(mc.value)
+        self.local = torch.as_tensor(_CAI(int(uc.value), int(n_keys)), device="cuda")
+
+    def reset(self):
+        """Every replica to CM_KEY_NONE (each rank writes its own; barrier before the next
+        call that reduces into it)."""
+        self.local.fill_((1 << 63) - 1)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.cm_mc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

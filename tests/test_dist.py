@@ -185,3 +185,48 @@ def test_winner_masks_two_ranks():
         assert np.array_equal(m0[b, 1].view(np.uint64), masks_u64(inst, o["S"]))
         seen += 1
     assert seen >= 2
+
+
+def _fd_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import importlib.util
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        spec = importlib.util.spec_from_file_location("cm_dist", os.path.join(root, "paper_1910_02653_b200", "dist.py"))
+        D = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(D)
+        fd = -1
+        if rank == 0:
+            r, w = os.pipe()
+            os.write(w, b"multicast handle of rank 0")
+            os.close(w)
+            fd = r
+        got = D.share_fd(fd, None)
+        data = os.read(got, 64) if rank != 0 else b""
+        out_q.put((rank, got >= 0, data))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_share_fd_over_unix_socket(world):
+    """The NVLS multicast handle's plumbing (dist.MulticastKeys): rank 0's file descriptor
+    reaches every other rank (SCM_RIGHTS over an abstract Unix socket whose name travels in the
+    process group) -- here a pipe whose contents the other ranks read back."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res)
+    # every non-zero rank reads the whole message through its own duplicate: the pipe is shared,
+    # so the reads split it; together they return it exactly once
+    got = b"".join(d for r, _, d in res if r != 0)
+    assert got == b"multicast handle of rank 0"
