@@ -283,7 +283,8 @@ const char* cm_policy_last_error(void);
  * granularity (cm_mc_size).  cm_mc_supported: 1 if the current device reports
  * CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED.  Errors: CM_EINVAL (arguments / call order),
  * CM_ECUDA (driver; cm_mc_last_error has the CUresult).  cm_mc_destroy unmaps and releases
- * (after a device synchronisation).  The object is exportable as a POSIX file descriptor.
+ * (after a device synchronisation).  A team (n_ranks > 1) is created exportable as a POSIX file
+ * descriptor; a team of one takes the first handle type the driver accepts (FABRIC, POSIX fd, none).
  */
 typedef struct cm_mc cm_mc;
 int32_t cm_mc_supported(void);
@@ -291,6 +292,7 @@ cm_status cm_mc_create(int64_t bytes, int32_t n_devices, cm_mc** out);
 cm_status cm_mc_export_fd(const cm_mc* m, int32_t* fd);
 cm_status cm_mc_import_fd(int32_t fd, int64_t bytes, cm_mc** out);
 int64_t cm_mc_size(const cm_mc* m);
+int32_t cm_mc_handle_type(const cm_mc* m);   /* the CUmemAllocationHandleType it was created with */
 cm_status cm_mc_add_device(cm_mc* m);
 cm_status cm_mc_bind(cm_mc* m, void** uc_ptr, void** mc_ptr);
 void cm_mc_destroy(cm_mc* m);

@@ -28,7 +28,7 @@ EXPORTS = ("cm_graph_create", "cm_graph_destroy", "cm_graph_n", "cm_graph_cost_b
            "cm_round_and_evaluate", "cm_workspace_bytes", "cm_sstar_floats", "cm_debug_trace", "cm_debug_last_launches", "cm_debug_cta_trace", "cm_debug_cta_trace_at",
            "cm_last_call_seq", "cm_stream_wait_call", "cm_key_idx_bits", "cm_decode_key", "cm_decode_batch_key", "cm_status_string", "cm_emit_plan", "cm_plan_last_error",
            "cm_policy_checkpoints", "cm_policy_sstar", "cm_policy_last_error",
-           "cm_mc_supported", "cm_mc_create", "cm_mc_export_fd", "cm_mc_import_fd", "cm_mc_size",
+           "cm_mc_supported", "cm_mc_create", "cm_mc_export_fd", "cm_mc_import_fd", "cm_mc_size", "cm_mc_handle_type",
            "cm_mc_add_device", "cm_mc_bind", "cm_mc_destroy", "cm_mc_last_error",
            "cm_last_error")
 
@@ -129,6 +129,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cm_mc_import_fd.restype = ctypes.c_int
     lib.cm_mc_size.argtypes = [P]
     lib.cm_mc_size.restype = ctypes.c_int64
+    lib.cm_mc_handle_type.argtypes = [P]
+    lib.cm_mc_handle_type.restype = ctypes.c_int32
     lib.cm_mc_add_device.argtypes = [P]
     lib.cm_mc_add_device.restype = ctypes.c_int
     lib.cm_mc_bind.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]

@@ -471,7 +471,11 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
     // slot predecessors must lie two windows back (W <= R / 2) or a warp blocked on one
     // window task can hold the ticket that would free its slot: clamped below.
     int64_t win = std::max<int64_t>(0, std::min<int64_t>(env_flag("CM_WIN", 0), 256));
-    int64_t ring_max = std::min<int64_t>(env_flag("CM_RING", 768), 4096);   // measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s
+    // ring slots: measured (n = 353): 256 -> 13.7, 512 -> 15.8, 768 -> 15.9 M cand/s, 1536 the same;
+    // small graphs gain from a deeper ring at the same bytes (VGG16, 44 KB slots: 768 -> 178.6,
+    // 4096 -> 210.5 M cand/s): default ~300 MB of slots, 768 .. 4096
+    const int64_t ring_auto = std::max<int64_t>(768, std::min<int64_t>(4096, (int64_t(300) << 20) / std::max<int64_t>(1, slot_bytes)));
+    int64_t ring_max = std::min<int64_t>(env_flag("CM_RING", (int)ring_auto), 4096);
     int64_t R = std::min<int64_t>(ring_max, units);
     auto ctl_bytes = [](int64_t r) { return (4 * cm2::fused_ctl_words(r) + 255) & ~int64_t(255); };
     // the graph's own workspace: two halves used alternately (CM_EVAL_OVERLAP needs the

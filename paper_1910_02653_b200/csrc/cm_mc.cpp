@@ -85,6 +85,7 @@ struct cm_mc {
   CUdeviceptr uc = 0, mcva = 0;          // unicast and multicast views of the replica
   size_t size = 0;                       // bytes, rounded up to the multicast granularity
   int device = -1;
+  int handle_type = 0;                   // CUmemAllocationHandleType the object was created with
   bool added = false, bound = false;
 };
 
@@ -106,23 +107,50 @@ cm_status cm_mc_create(int64_t bytes, int32_t n_devices, cm_mc** out) {
   if (!out || bytes <= 0 || n_devices < 1) return mc_fail(CM_EINVAL, "bad arguments");
   *out = nullptr;
   if (!drv().ok()) return mc_fail(CM_ECUDA, "multicast driver entry points unavailable");
+  CUdevice dev;
+  int ord;
+  cm_status st = current_device(&dev, &ord);
+  if (st != CM_OK) return st;
+  // size: a multiple of both the multicast and the physical allocation granularity (minimum)
+  CUmemAllocationProp ap = {};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = ord;
+  size_t ag = 0;
+  CUresult r = drv().mem_gran(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMemGetAllocationGranularity");
   CUmulticastObjectProp prop = {};
   prop.numDevices = (unsigned)n_devices;
-  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;      // exportable (a team of one: unused)
   prop.size = (size_t)bytes;
-  size_t gran = 0;
-  CUresult r = drv().mc_gran(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED);
-  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMulticastGetGranularity");
-  prop.size = ((size_t)bytes + gran - 1) / gran * gran;
-  cm_mc* m = new cm_mc;
-  m->size = prop.size;
-  r = drv().mc_create(&m->mc, &prop);
-  if (r != CUDA_SUCCESS) {
-    delete m;
-    return cu_fail(r, "cuMulticastCreate");
+  // a team: exportable as a POSIX fd (the other ranks import it).  A team of one needs no
+  // export; it takes the first handle type the driver accepts (measured on the B200 boxes: only
+  // FABRIC -- POSIX fd and none give CUDA_ERROR_INVALID_VALUE there)
+  const CUmemAllocationHandleType team[] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR};
+  const CUmemAllocationHandleType solo[] = {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                            CU_MEM_HANDLE_TYPE_NONE};
+  const int n_ht = n_devices > 1 ? 1 : 3;
+  for (int i = 0; i < n_ht; ++i) {
+    const CUmemAllocationHandleType ht = n_devices > 1 ? team[i] : solo[i];
+    prop.handleTypes = ht;
+    size_t mg = 0;
+    r = drv().mc_gran(&mg, &prop, CU_MULTICAST_GRANULARITY_MINIMUM);
+    if (r != CUDA_SUCCESS) continue;
+    size_t g = mg;
+    while (g % ag) g += mg;                                         // lcm (both powers of two in practice)
+    prop.size = ((size_t)bytes + g - 1) / g * g;
+    CUmemGenericAllocationHandle h = 0;
+    r = drv().mc_create(&h, &prop);
+    if (r == CUDA_SUCCESS) {
+      cm_mc* m = new cm_mc;
+      m->mc = h;
+      m->size = prop.size;
+      m->handle_type = (int)ht;
+      *out = m;
+      return CM_OK;
+    }
   }
-  *out = m;
-  return CM_OK;
+  return mc_fail(CM_ECUDA, "cuMulticastCreate: CUresult " + std::to_string((int)r) + " for every handle type (size " +
+                               std::to_string(prop.size) + ", alloc granularity " + std::to_string(ag) + ")");
 }
 
 cm_status cm_mc_export_fd(const cm_mc* m, int32_t* fd) {
@@ -152,6 +180,8 @@ cm_status cm_mc_import_fd(int32_t fd, int64_t bytes, cm_mc** out) {
 
 int64_t cm_mc_size(const cm_mc* m) { return m ? (int64_t)m->size : -1; }
 
+int32_t cm_mc_handle_type(const cm_mc* m) { return m ? m->handle_type : -1; }
+
 cm_status cm_mc_add_device(cm_mc* m) {
   if (!m || m->added) return mc_fail(CM_EINVAL, "NULL or device already added");
   CUdevice dev;
@@ -171,7 +201,7 @@ cm_status cm_mc_bind(cm_mc* m, void** uc_ptr, void** mc_ptr) {
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = m->device;
   size_t g = 0;
-  CUresult r = d.mem_gran(&g, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  CUresult r = d.mem_gran(&g, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuMemGetAllocationGranularity");
   if (m->size % g) return mc_fail(CM_EINVAL, "multicast size not a multiple of the allocation granularity");
   if ((r = d.mem_create(&m->mem, m->size, &ap, 0)) != CUDA_SUCCESS) return cu_fail(r, "cuMemCreate");
