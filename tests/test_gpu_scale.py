@@ -6,7 +6,8 @@
   against the CPU oracle -- the first 1 000, unit boundaries, the last unit and 1 000 random
   ones -- and every per-budget key against the call's own per-candidate outputs.  A second
   check compares ALL candidates of the fused launch with the two-kernel pipeline
-  (CM_FUSED=0): a detector for ring hand-off races, not a parity claim.
+  (CM_FUSED=0): a detector for ring hand-off races, not a parity claim.  The same for
+  randomized rounding at bench.py --samples 1 / 4's launch.
 - a8: the CUDA path over P contiguous index_base shards,
   MIN-reduced, equals the unsharded call and the oracle's best_per_budget (Alg. 2 +
   budget row; SURVEY invariant 9, shard invariance); the winners'
@@ -66,10 +67,16 @@ def oracle_keys(peaks, costs, budgets, bits, index_base=0):
 
 
 @pytest.mark.timeout(1800)
-@pytest.mark.parametrize("layout", ["blk", "dense"])
+@pytest.mark.parametrize("layout,ring", [("blk", None), ("dense", None), ("blk", 256)])
 @pytest.mark.parametrize("cfg", ["resnet50", "vgg16", "unet", "mobilenet", "fcn8"])
-def test_bench_config_full_launch(cfg, layout, env_var):
+def test_bench_config_full_launch(cfg, layout, ring, env_var):
+    """ring: CM_RING slots (None: the library's default, ~300 MB of slots -- every unit of a
+    VGG16 call, so only the forced 256-slot ring makes its claim-8 producers wrap)."""
     import torch
+    if ring is not None:
+        if cfg not in ("vgg16", "unet"):
+            pytest.skip("forced ring depth: small graphs only (the default already wraps at n >= 353)")
+        env_var(CM_RING=ring)
     import paper_1910_02653_b200 as cm
     from workloads.device_gen import DeviceGenerator
     g, fam, thetas, budgets, N = bench.build_workload(cfg)
@@ -114,6 +121,63 @@ def test_bench_config_full_launch(cfg, layout, env_var):
     for s in sample:
         for j in range(nt):
             c = s * nt + j
+            w = want[s][j]
+            for peak, cost, _ in got:
+                if (int(peak[c]), int(cost[c])) != (w[0], w[1]):
+                    bad.append((s, j, int(peak[c]), int(cost[c]), w[0], w[1]))
+    assert not bad, bad[:10]
+    graph.close()
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("samples,N", [(1, 125000), (4, 31250)])
+def test_bench_launch_randomized(samples, N, env_var):
+    """Randomized rounding (R1) at bench.py --samples K's launch: ResNet-50, device-
+    generated G1 S* in the blocked layout, bench's seed (also the Philox key), three overlapped
+    calls on two alternating output sets with in-kernel key init.  >= 2 000 S* (x K samples)
+    against the oracle's evaluate_randomized; every candidate of the fused launch against the
+    two-kernel pipeline (ring-race detector); keys against the call's own outputs."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    g, fam, _, budgets, _ = bench.build_workload("resnet50")
+    dev = torch.device("cuda:0")
+    dg = DeviceGenerator(g, fam, BENCH_SEED, layout="blk")
+    buf = torch.empty(dg.shape(N), dtype=torch.float32, device=dev)
+    dg.fill(buf, 0)
+    graph = cm.Graph.from_workload(g)
+    bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
+    nc = N * samples
+    sets = [{k: torch.zeros(m, dtype=torch.int64, device=dev) for k, m in
+             (("peak", nc), ("cost", nc), ("key", len(budgets)))} for _ in range(2)]
+    torch.cuda.synchronize()
+    for step in range(3):
+        o = sets[step % 2]
+        out = cm.round_and_evaluate(graph, buf, None, bu, best_key=o["key"], peak=o["peak"], cost=o["cost"],
+                                    total_candidates=nc, init_keys=True, overlap=True, layout="blk",
+                                    samples=samples, seed=BENCH_SEED)
+        assert cm.debug_last_launches() == 1
+    torch.cuda.synchronize()
+    bits = out["idx_bits"]
+    got = [(o["peak"].cpu().numpy(), o["cost"].cpu().numpy(), o["key"].cpu().numpy()) for o in sets]
+    env_var(CM_FUSED=0)
+    ref = cm.round_and_evaluate(graph, buf, None, bu, total_candidates=nc, layout="blk", samples=samples,
+                                seed=BENCH_SEED)
+    torch.cuda.synchronize()
+    env_var(CM_FUSED=1)
+    rp, rc = ref["peak"].cpu().numpy(), ref["cost"].cpu().numpy()
+    del buf, ref
+    torch.cuda.empty_cache()
+    for peak, cost, key in got:
+        assert np.array_equal(peak, rp) and np.array_equal(cost, rc)
+        assert list(key) == keys_of(peak, cost, budgets, bits)
+    sample = boundary_sample(N)
+    assert len(sample) >= 2000
+    want = oracle_many(g, fam, BENCH_SEED, sample, samples=samples, rseed=BENCH_SEED)
+    bad = []
+    for s in sample:
+        for j in range(samples):
+            c = s * samples + j
             w = want[s][j]
             for peak, cost, _ in got:
                 if (int(peak[c]), int(cost[c])) != (w[0], w[1]):
