@@ -454,6 +454,12 @@ __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t 
 #ifndef CM_BLK_EVICT_FIRST
 #define CM_BLK_EVICT_FIRST 1
 #endif
+// K1 software pipelining (block w's finish after block w+1's pack): measured 0.5-2 % slower
+// on every config (ResNet-50 21.40 vs 21.44, VGG16 209 vs 214, rand1 9.80 vs 9.96 M cand/s;
+// profiles r2au) -- the rounding warps are not latency-bound here: off
+#ifndef CM_K1_PIPE
+#define CM_K1_PIPE 0
+#endif
 
 // K1 for the blocked layout (CM_LAYOUT_BLK): the same per-block steps as k1_body, with the
 // bookkeeping hoisted out of the block loop -- a group's row masks, store pointers and table
@@ -565,9 +571,12 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
       int64_t mass[NT];
 #pragma unroll
       for (int j = 0; j < NT; ++j) mass32[j] = 0, mass[j] = 0;
-      // one block: xp holds this lane's row (elements 2k, 2k+1 in xp[k]), w its node block
-      auto block = [&](const uint64_t (&xp)[16], uint32_t rmask, int w) {
-        uint32_t word[NT];
+      // one block in two halves: pack (xp holds this lane's row, elements 2k, 2k+1 in xp[k]) ->
+      // the row word; finish -> the stage-sliced column word (transpose), row 32(g+1)'s word and
+      // the row's checkpoint mass.  CM_K1_PIPE: block w's finish runs after block w+1's pack, so
+      // the two dependency chains (FADD2 / funnel shifts, SHFL transpose / mass lookups) of
+      // consecutive blocks interleave in one basic block.
+      auto pack = [&](const uint64_t (&xp)[16], uint32_t rmask, int w, uint32_t (&word)[NT]) {
         if (RAND) {
           rand_words<NT>(word, xp, w, rq, sg, p);
 #pragma unroll
@@ -576,6 +585,9 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
 #pragma unroll
           for (int j = 0; j < NT; ++j) word[j] = pack_sub(xp, tt[j]) & rmask;
         }
+      };
+      const int64_t* tw64 = p.nib;                                  // int64 tables of the next block
+      auto finish = [&](const uint32_t (&word)[NT]) {
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           if (wbrow) browp[j * cs] = word[j];
@@ -601,7 +613,6 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
             mass32[j] += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
           }
         } else {
-          const int64_t* tw64 = p.nib + 128 * w;
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             int64_t ms = 0;
@@ -612,10 +623,14 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
         }
 #endif
         tb += 512u;
+        tw64 += 128;
       };
       // one body for every block (the hot loop stays small next to K2's in the instruction
       // cache); only the 8 shared loads depend on the block's form
       const bool bfull = g < Gr - 1 || h_last == 32;
+      uint32_t pend[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) pend[j] = 0u;
       for (int w = 0; w <= g; ++w) {
         const uint32_t st0 = wait_block();
         const uint32_t rb = st0 + 16u * (uint32_t)lane;
@@ -645,8 +660,17 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
             b += max(0, h_last - 4 * c);
           }
         }
-        block(xp, w < g ? rm_off : rm_diag, w);
+        uint32_t word[NT];
+        pack(xp, w < g ? rm_off : rm_diag, w, word);
+        if (CM_K1_PIPE) {
+          if (w > 0) finish(pend);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) pend[j] = word[j];
+        } else {
+          finish(word);
+        }
       }
+      if (CM_K1_PIPE) finish(pend);
       if (rq < n) {
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
