@@ -409,9 +409,53 @@ __device__ __forceinline__ void philox_xk(uint4 (&c)[KB], uint32_t k0, uint32_t 
                         (uint32_t)p0[b]);
   }
 }
+// CM_RAND_CMP 1: the same exact compare in integers -- C = ceil(x 2^32) once per element
+// (cvt.rpi.u32.f32 of the exact x 2^32, saturating: x <= 0 and NaN -> 0, never; x >= 1 ->
+// 2^32 - 1, so [x >= 1] is OR-ed in from one packed compare against nextbelow(1)), and
+// [w < C] = [w < x 2^32] since C is the least integer >= x 2^32.  Per sample the carry of
+// w - C is shifted into the word (sub.cc + addc: one ALU IADD3 and one IMAD.X on the FMA pipe
+// instead of I2FP + funnel shift; the F2I runs on the XU pipe once per element).  On sm_100a
+// the carry after sub.cc is the no-borrow flag [w >= C] (the other polarity fails the parity
+// tests), so the word is complemented.  Bit-exact (profiles r2aw, r2ax) but measured slower at
+// 1 and 2 samples (9.68 / 9.99 vs 9.96 / 10.24 M cand/s) and +1 % at 4: off (0: fp32 sign form).
+#ifndef CM_RAND_CMP
+#define CM_RAND_CMP 0
+#endif
 template <int NT>
 __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t (&xp)[16], int w, int rq, uint32_t sg,
                                            const RoundParams& p) {
+  if constexpr (CM_RAND_CMP == 1) {
+    uint32_t C[32];                                                 // ceil(x 2^32), saturated
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      uint64_t X;
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(X) : "l"(xp[k]), "l"(0x4f8000004f800000ull));
+      asm("cvt.rpi.u32.f32 %0, %1;" : "=r"(C[2 * k]) : "f"(__uint_as_float((uint32_t)X)));
+      asm("cvt.rpi.u32.f32 %0, %1;" : "=r"(C[2 * k + 1]) : "f"(__uint_as_float((uint32_t)(X >> 32))));
+    }
+    const uint32_t ge1 = pack_sub(xp, 0x3f7fffff3f7fffffull);      // x > nextbelow(1) = x >= 1
+    auto bpack4 = [&](uint32_t& acc, const uint4& o, int e0) {      // elements e0 .. e0 + 3, descending
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 3; e >= 0; --e)
+        asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}"
+            : "+r"(acc) : "r"(ow[e]), "r"(C[e0 + e]));
+    };
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      uint32_t hi = 0u, lo = 0u;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        uint4 o[2] = {make_uint4((uint32_t)(8 * w + q + 4), (uint32_t)rq, sg, (uint32_t)(p.th0 + j)),
+                      make_uint4((uint32_t)(8 * w + q), (uint32_t)rq, sg, (uint32_t)(p.th0 + j))};
+        philox_xk<2>(o, p.key0, p.key1);
+        bpack4(hi, o[0], 4 * (q + 4));
+        bpack4(lo, o[1], 4 * q);
+      }
+      word[j] = ~((hi << 16) | lo) | ge1;                          // the shifted-in bits are [w >= C]
+    }
+    return;
+  }
   uint64_t X[16];                                                   // x 2^32, elements 2k, 2k+1
 #pragma unroll
   for (int k = 0; k < 16; ++k) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(X[k]) : "l"(xp[k]), "l"(0x4f8000004f800000ull));
