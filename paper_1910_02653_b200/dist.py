@@ -113,8 +113,9 @@ class MulticastKeys:
 
     .local  torch int64 tensor: this GPU's replica (pass as best_key; read after a barrier)
     .mc     int: the multicast address (pass as best_key_mc)
-    Collective over the group (one process per GPU).  Raises CMError where the device or the
-    driver offers no multicast (cm_mc_supported() == 0)."""
+    Collective over the group (one process per GPU).  Raises CMError on every rank if any
+    rank's stage fails (e.g. no multicast object on the box), instead of leaving the others
+    waiting in the next collective."""
 
     def __init__(self, n_keys: int, group=None):
         import ctypes
@@ -122,36 +123,49 @@ class MulticastKeys:
         import torch.distributed as dist
         from . import CMError, _lib
         P = ctypes.c_void_p
-
-        def _check(status, where):
-            if status != 0:
-                raise CMError(status, where + ": " + _lib.cm_mc_last_error().decode())
         world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         rank = dist.get_rank(group) if world > 1 else 0
+        src = (dist.get_global_rank(group, 0) if group is not None else 0) if world > 1 else 0
         self._lib = _lib
+        self.handle = None
         h = P()
+
+        def step(fn, where):
+            """Run one stage on this rank; every rank learns whether all succeeded (a failed
+            rank must not leave the others waiting in the next collective)."""
+            err = ""
+            try:
+                st = fn()
+                if st:
+                    err = f"{where}: {_lib.cm_status_string(st).decode()}: {_lib.cm_mc_last_error().decode()}"
+            except Exception as ex:  # pragma: no cover
+                err = f"{where}: {ex!r}"
+            errs = [err]
+            if world > 1:
+                errs = [None] * world
+                dist.all_gather_object(errs, err, group=group)
+            bad = [e for e in errs if e]
+            if bad:
+                self.close()
+                raise CMError(5, "MulticastKeys: " + "; ".join(bad))
+
         nbytes = 8 * int(n_keys)
-        if rank == 0:
-            _check(_lib.cm_mc_create(nbytes, world, ctypes.byref(h)), "cm_mc_create")
+        fd = ctypes.c_int32(-1)
+        step(lambda: (_lib.cm_mc_create(nbytes, world, ctypes.byref(h)) or
+                      (world > 1 and _lib.cm_mc_export_fd(h, ctypes.byref(fd)))) if rank == 0 else 0,
+             "cm_mc_create / export")
+        self.handle = h if rank == 0 else None
         if world > 1:
-            fd = ctypes.c_int32(-1)
             size = [int(_lib.cm_mc_size(h)) if rank == 0 else 0]
-            if rank == 0:
-                _check(_lib.cm_mc_export_fd(h, ctypes.byref(fd)), "cm_mc_export_fd")
-            dist.broadcast_object_list(size, src=dist.get_global_rank(group, 0) if group is not None else 0,
-                                       group=group)
+            dist.broadcast_object_list(size, src=src, group=group)
             got = share_fd(fd.value if rank == 0 else -1, group)
-            if rank != 0:
-                _check(_lib.cm_mc_import_fd(got, size[0], ctypes.byref(h)), "cm_mc_import_fd")
-        self.handle = h
-        _check(_lib.cm_mc_add_device(h), "cm_mc_add_device")
-        if world > 1:
-            dist.barrier(group=group)           # every device added before any binds
+            step(lambda: _lib.cm_mc_import_fd(got, size[0], ctypes.byref(h)) if rank != 0 else 0, "cm_mc_import_fd")
+            self.handle = h
+        step(lambda: _lib.cm_mc_add_device(h), "cm_mc_add_device")   # all added before any binds
         uc, mc = P(), P()
-        _check(_lib.cm_mc_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "cm_mc_bind")
-        if world > 1:
-            dist.barrier(group=group)
+        step(lambda: _lib.cm_mc_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "cm_mc_bind")
         self.mc = int(mc.value)
+        # a view of the replica: keep this object alive while the tensor is used
         self.local = torch.as_tensor(_CAI(int(uc.value), int(n_keys)), device="cuda")
 
     def reset(self):

@@ -230,3 +230,37 @@ def test_share_fd_over_unix_socket(world):
     # so the reads split it; together they return it exactly once
     got = b"".join(d for r, _, d in res if r != 0)
     assert got == b"multicast handle of rank 0"
+
+
+def _mc_fail_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1910_02653_b200 as cm
+        from paper_1910_02653_b200.dist import MulticastKeys
+        try:
+            MulticastKeys(16)
+            out_q.put((rank, "created"))
+        except cm.CMError as ex:
+            out_q.put((rank, "raised: " + str(ex)[:200]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_multicast_keys_fail_together_without_gpu():
+    """dist.MulticastKeys is collective: where rank 0 cannot create the multicast object (here:
+    no GPU at all), every rank raises CMError -- none is left waiting in the next collective."""
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check of the failure path")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mc_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(msg.startswith("raised") and "cm_mc_create" in msg for _, msg in res), res
