@@ -171,9 +171,9 @@ EncodeTiledFn encode_tiled() {
 
 // Per-candidate workspace bytes of one chunk buffer: K1 output block + K2 partials.
 int64_t cand_bytes(int n, bool m32) { return 4 * (int64_t)cm2::cand_words(n, m32) + 16 * (int64_t)((n + 31) / 32); }
-size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256) {
+size_t scan_warp_bytes(int n_slot, bool s32, bool tm, int tcols = 256, int q = cm2::kSnRing) {
   const int spill = std::max(0, n_slot - (tm ? tcols : 0));        // A' slots kept in shared memory
-  return (size_t)cm2::scan_e_bytes(s32) + (size_t)4 * 32 * spill;   // E (+ staged int32 masses), spill
+  return (size_t)cm2::scan_e_bytes(s32, q) + (size_t)4 * 32 * spill;   // E (+ staged int32 masses, Sn ring), spill
 }
 // CM_TRACE=1: record timing events around every K1 (round stream) and K2+K3 (caller stream)
 // launch of the next call; cm_debug_trace() returns their offsets (debug / overlap check).
@@ -462,8 +462,9 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   if ((g->scan32 || !rnd) && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
     const int nt = a->n_theta;
     const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
-    const size_t wbf = scan_warp_bytes(g->n_slot, g->scan32, true, cm2::kFusedTmemCols);
-    const size_t smemf = k1b + fixed + wbf * cm2::kFusedScanWarps + 1024;
+    const size_t wbf = scan_warp_bytes(g->n_slot, g->scan32, true, cm2::fused_tmem_cols(nt, rnd),
+                                       cm2::fused_sn_ring(nt, rnd));
+    const size_t smemf = k1b + fixed + wbf * cm2::fused_scan_warps(nt, rnd) + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
     // scan-task tickets: unit-major (default) or windows of CM_WIN units, group-major inside
@@ -498,7 +499,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
           e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fused_kernel)");
       }
-      const int threads = 32 * cm2::fused_warps(nt);
+      const int threads = 32 * cm2::fused_warps(nt, rnd);
       int occf = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, fn, threads, smemf);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy(fused_kernel)");

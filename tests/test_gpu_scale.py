@@ -130,6 +130,61 @@ def test_bench_config_full_launch(cfg, layout, ring, env_var):
 
 
 @pytest.mark.timeout(1800)
+@pytest.mark.parametrize("thetas", [[0.2, 0.4, 0.5, 0.7], [0.5, 0.3]])
+def test_bench_launch_multi_threshold(thetas, env_var):
+    """bench.py --thetas launch (the fused instances with 2-4 thresholds run 12 scan warps,
+    setmaxnreg-rebalanced, 4-quad Sn rings): ResNet-50, 125 000 device-generated G1 S*, blocked
+    layout, three overlapped calls; >= 2 000 S* x N_theta against the oracle, every candidate
+    against the two-kernel pipeline, keys against the call's own outputs."""
+    import torch
+    import paper_1910_02653_b200 as cm
+    from workloads.device_gen import DeviceGenerator
+    g, fam, _, budgets, N = bench.build_workload("resnet50")
+    nt = len(thetas)
+    dev = torch.device("cuda:0")
+    dg = DeviceGenerator(g, fam, BENCH_SEED, layout="blk")
+    buf = torch.empty(dg.shape(N), dtype=torch.float32, device=dev)
+    dg.fill(buf, 0)
+    graph = cm.Graph.from_workload(g)
+    th = torch.tensor(thetas, dtype=torch.float32, device=dev)
+    bu = torch.tensor(budgets, dtype=torch.int64, device=dev)
+    nc = N * nt
+    sets = [{k: torch.zeros(m, dtype=torch.int64, device=dev) for k, m in
+             (("peak", nc), ("cost", nc), ("key", len(budgets)))} for _ in range(2)]
+    torch.cuda.synchronize()
+    for step in range(3):
+        o = sets[step % 2]
+        out = cm.round_and_evaluate(graph, buf, th, bu, best_key=o["key"], peak=o["peak"], cost=o["cost"],
+                                    total_candidates=nc, init_keys=True, overlap=True, layout="blk")
+        assert cm.debug_last_launches() == 1
+    torch.cuda.synchronize()
+    bits = out["idx_bits"]
+    got = [(o["peak"].cpu().numpy(), o["cost"].cpu().numpy(), o["key"].cpu().numpy()) for o in sets]
+    env_var(CM_FUSED=0)
+    ref = cm.round_and_evaluate(graph, buf, th, bu, total_candidates=nc, layout="blk")
+    torch.cuda.synchronize()
+    env_var(CM_FUSED=1)
+    rp, rc = ref["peak"].cpu().numpy(), ref["cost"].cpu().numpy()
+    del buf, ref
+    torch.cuda.empty_cache()
+    for peak, cost, key in got:
+        assert np.array_equal(peak, rp) and np.array_equal(cost, rc)
+        assert list(key) == keys_of(peak, cost, budgets, bits)
+    sample = boundary_sample(N)
+    want = oracle_many(g, fam, BENCH_SEED, sample, thetas)
+    bad = []
+    for s in sample:
+        for j in range(nt):
+            c = s * nt + j
+            w = want[s][j]
+            for peak, cost, _ in got:
+                if (int(peak[c]), int(cost[c])) != (w[0], w[1]):
+                    bad.append((s, j, int(peak[c]), int(cost[c]), w[0], w[1]))
+    assert not bad, bad[:10]
+    graph.close()
+
+
+@pytest.mark.timeout(1800)
 @pytest.mark.parametrize("samples,N", [(1, 125000), (4, 31250)])
 def test_bench_launch_randomized(samples, N, env_var):
     """Randomized rounding (R1) at bench.py --samples K's launch: ResNet-50, device-
