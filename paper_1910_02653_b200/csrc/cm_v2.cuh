@@ -1828,8 +1828,16 @@ struct K1Ring {
 #ifndef CM_SN_RING_N
 #define CM_SN_RING_N 4
 #endif
-__host__ __device__ constexpr int fused_scan_warps(int nt, bool rand) { return nt >= 2 && !rand ? CM_KF2N : CM_KF2; }
-__host__ __device__ constexpr int fused_sn_ring(int nt, bool rand) { return nt >= 2 && !rand ? CM_SN_RING_N : kSnRing; }
+// randomized rounding with 2-4 samples: scan warps (tuning; its K1 keeps CM_FUSED_K1_REGS_RAND)
+#ifndef CM_KF2N_RAND
+#define CM_KF2N_RAND CM_KF2
+#endif
+__host__ __device__ constexpr int fused_scan_warps(int nt, bool rand) {
+  return nt >= 2 ? (rand ? CM_KF2N_RAND : CM_KF2N) : CM_KF2;
+}
+__host__ __device__ constexpr int fused_sn_ring(int nt, bool rand) {
+  return fused_scan_warps(nt, rand) > 8 ? CM_SN_RING_N : kSnRing;
+}
 #ifndef CM_FUSED_TMEM
 #define CM_FUSED_TMEM 512
 #endif
@@ -1851,11 +1859,15 @@ __host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, boo
 #ifndef CM_FUSED_K1_REGS
 #define CM_FUSED_K1_REGS 72
 #endif
+#ifndef CM_FUSED_K1_REGS_RAND
+#define CM_FUSED_K1_REGS_RAND 88
+#endif
+__host__ __device__ constexpr int fused_k1_regs(bool rand) { return rand ? CM_FUSED_K1_REGS_RAND : CM_FUSED_K1_REGS; }
 __host__ __device__ constexpr int fused_launch_regs(int nt, bool rand) {
   return (65536 / (32 * fused_warps(nt, rand))) / 8 * 8;
 }
 __host__ __device__ constexpr int fused_k2_regs(int nt, bool rand) {
-  return (fused_launch_regs(nt, rand) + k1_warps(nt) * (fused_launch_regs(nt, rand) - CM_FUSED_K1_REGS) /
+  return (fused_launch_regs(nt, rand) + k1_warps(nt) * (fused_launch_regs(nt, rand) - fused_k1_regs(rand)) /
           fused_scan_warps(nt, rand)) / 8 * 8;
 }
 
@@ -1909,10 +1921,10 @@ __global__ void __launch_bounds__(32 * fused_warps(NT, RAND), CM_FUSED_MINB) fus
 
   constexpr bool kRebal = fused_warps(NT, RAND) > 16;
   static_assert(!kRebal || (KF1 % 4 == 0 && KF2 % 4 == 0 && !kK1High), "warpgroup roles");
-  static_assert(!kRebal || (CM_FUSED_K1_REGS <= fused_launch_regs(NT, RAND) && fused_k2_regs(NT, RAND) <= 256),
+  static_assert(!kRebal || (fused_k1_regs(RAND) <= fused_launch_regs(NT, RAND) && fused_k2_regs(NT, RAND) <= 256),
                 "register pool");
   if (kK1High ? warp >= KF2 : warp < KF1) {                         // ---- rounding (K1) warps
-    if constexpr (kRebal) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(CM_FUSED_K1_REGS));
+    if constexpr (kRebal) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(fused_k1_regs(RAND)));
     __shared__ int sq[KF1][8];
     const int w1 = kK1High ? warp - KF2 : warp;
     const K1Ring hk{fp.ring, fp.slot_words, fp.n_slots, fp.n_theta, fp.rp.cs, fp.ctl, fp.claim, fp.n_sstar};
