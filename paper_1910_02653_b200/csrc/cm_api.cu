@@ -417,6 +417,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   // an S* whose rows' 128-byte windows stay inside the buffer: (s + 1) stride + 32 <= N stride
   rp.g4_end = a->sstar_stride > 0 ? std::max<int64_t>(0, (int64_t)a->n_sstar - (32 + a->sstar_stride - 1) / a->sstar_stride)
                                   : 0;
+  rp.rtab = 0;                                        // the fused blocked randomized path sets it
   rp.key0 = (uint32_t)(a->seed & 0xffffffffu);
   rp.key1 = (uint32_t)(a->seed >> 32);
   rp.s0 = (uint32_t)((uint64_t)(a->index_base / a->n_theta) & 0xffffffffu);
@@ -461,10 +462,13 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
   // ---- fused persistent path (one launch; see cm2::fused_kernel) ----
   if ((g->scan32 || !rnd) && tm && a->n_theta <= 4 && env_flag("CM_FUSED", 1)) {
     const int nt = a->n_theta;
-    const size_t k1b = cm2::fused_k1_bytes(nt, nib_staged, bulk);
     const size_t wbf = scan_warp_bytes(g->n_slot, g->scan32, true, cm2::fused_tmem_cols(nt, rnd),
                                        cm2::fused_sn_ring(nt, rnd));
-    const size_t smemf = k1b + fixed + wbf * cm2::fused_scan_warps(nt, rnd) + 1024;
+    // randomized rounding, blocked layout: the fused kernel's rounding warps keep per-S* Philox
+    // tables ([G][8][nt] x 16 bytes per K1 warp) in shared memory (if they do not fit, the
+    // smem check below sends the call to the two-kernel pipeline)
+    const int rtab = (rnd && a->layout == CM_LAYOUT_BLK) ? G * 8 * nt * 16 : 0;
+    const size_t smemf = cm2::fused_k1_bytes(nt, nib_staged, bulk, rtab) + fixed + wbf * cm2::fused_scan_warps(nt, rnd) + 1024;
     const int64_t slot_bytes = 32 * (int64_t)nt * cand_bytes(n, m32);
     const int64_t units = ((int64_t)a->n_sstar + 31) / 32;
     // scan-task tickets: unit-major (default) or windows of CM_WIN units, group-major inside
@@ -521,6 +525,7 @@ cm_status launch_v2(cm_graph* g, const cm_eval_args* a, cudaStream_t st, int32_t
         rp.nt = nt;
         rp.sn = nullptr;
         fp.rp = rp;
+        fp.rp.rtab = rtab;
         fp.sp = sp;
         fp.sp.warp_bytes = (int32_t)wbf;
         fp.qp = qp;

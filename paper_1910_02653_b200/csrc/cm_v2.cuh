@@ -163,6 +163,7 @@ struct RoundParams {
   uint32_t s0;                // global index of batch S* 0 (mod 2^32)
   int32_t g4;                 // tri4: tile::gather4 through the 16-byte-unit tensor map (else per-row copies)
   int64_t g4_end;             // batch-relative: S* from here on take per-row copies (window past the end)
+  int32_t rtab;               // RAND, fused blocked path: bytes per K1 warp of the per-S* Philox table (0: none)
 };
 
 // w |= (x[q] > th) << q for q = Q0 .. Q0+15 (strict fp32 compare, NaN -> 0): a setp and a
@@ -323,6 +324,10 @@ __host__ __device__ constexpr size_t k1_cols_off(int nt, bool bulk = false) {
 __host__ __device__ constexpr size_t k1_nib_off(int nt, bool bulk = false) {
   return (k1_cols_off(nt, bulk) + (size_t)k1_warps(nt) * nt * 128 + 511) & ~(size_t)511;
 }
+// the Philox tables [K1 warp][rtab bytes], after the staged mass tables
+__host__ __device__ constexpr size_t k1_rtab_off(int nt, int nib_entries, bool bulk) {
+  return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 15) / 16 * 16;
+}
 // dynamic bytes to request: + 1024 slack for aligning the base
 __host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries, bool bulk = false) {
   return k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1024;
@@ -341,6 +346,7 @@ __host__ __device__ constexpr size_t k1_smem_bytes(int nt, int nib_entries, bool
 // word of S* s is written.  K1Plain: the chunk buffer of the two-kernel pipeline.
 // first() / next(s) give the S* a warp processes, in order (K1Plain: a static stride).
 struct K1Plain {
+  static constexpr bool kTab = false;                             // no per-S* Philox table (rtab)
   uint32_t* sn;
   int32_t n_theta, th0, cs;
   int32_t wid, nw;
@@ -421,9 +427,100 @@ __device__ __forceinline__ void philox_xk(uint4 (&c)[KB], uint32_t k0, uint32_t 
 #ifndef CM_RAND_CMP
 #define CM_RAND_CMP 0
 #endif
-template <int NT>
+// Philox4x32-10 rounds 3..9 (0-based) of KB blocks from the state after round 2 (k0, k1 the base key)
+template <int KB>
+__device__ __forceinline__ void philox_tail_xk(uint4 (&c)[KB], uint32_t k0, uint32_t k1) {
+  k0 += 2u * 0x9E3779B9u;
+  k1 += 2u * 0xBB67AE85u;
+#pragma unroll
+  for (int r = 3; r < 10; ++r) {
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+    uint64_t p0[KB], p1[KB];
+#pragma unroll
+    for (int b = 0; b < KB; ++b) {
+      p0[b] = (uint64_t)0xD2511F53u * c[b].x;
+      p1[b] = (uint64_t)0xCD9E8D57u * c[b].z;
+    }
+#pragma unroll
+    for (int b = 0; b < KB; ++b)
+      c[b] = make_uint4((uint32_t)(p1[b] >> 32) ^ c[b].y ^ k0, (uint32_t)p1[b], (uint32_t)(p0[b] >> 32) ^ c[b].w ^ k1,
+                        (uint32_t)p0[b]);
+  }
+}
+// The per-S* Philox table (RoundParams::rtab): rounds 0-2 of a block depend on the lane only
+// through its row rq (counter word 1, entering round 0 by XOR); the rest of rounds 0-2 depends
+// on (node block w, q4, sample j) and the S* number, so each warp computes it once per S* for
+// all (w, q4, j), lane-parallel: entry {w1 ^ k1_1, y2 ^ k0_2, hi(M0 x2) ^ k1_2, lo(M0 x2)} with
+// (x1, y1, z1, w1) the round-0 output without the row, y2 = lo(M1 z1), x2 = hi(M1 z1) ^ y1 ^ k0_1.
+// A lane then finishes round 1 with P = M0 x1 (x1 = hi(M1 S*) ^ row ^ k0, once per group) and
+// round 2 with one IMAD.WIDE: z2 = hi(P) ^ A, x3 = hi(M1 z2) ^ B, y3 = lo(M1 z2), z3 = C ^ lo(P),
+// w3 = D -- the same bits as the plain block (oracle R1), ~2 IMAD.WIDE and ~4 ALU ops fewer.
+__device__ __forceinline__ void rand_table_build(uint32_t tab, int Gr, int NTs, uint32_t sg, const RoundParams& p) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t k0 = p.key0, k1 = p.key1;
+  const uint64_t q2 = (uint64_t)0xCD9E8D57u * sg;
+  const uint32_t y1 = (uint32_t)q2;
+  const int ne = Gr * 8 * NTs;
+  for (int e = lane; e < ne; e += 32) {
+    const int j = e % NTs, wq = e / NTs;                            // wq = 8 w + q4
+    const uint64_t p0 = (uint64_t)0xD2511F53u * (uint32_t)wq;
+    const uint32_t z1 = (uint32_t)(p0 >> 32) ^ (uint32_t)(p.th0 + j) ^ k1, w1 = (uint32_t)p0;
+    const uint64_t q = (uint64_t)0xCD9E8D57u * z1;
+    const uint32_t x2 = (uint32_t)(q >> 32) ^ y1 ^ (k0 + 0x9E3779B9u);
+    const uint64_t r = (uint64_t)0xD2511F53u * x2;
+    const uint32_t A = w1 ^ (k1 + 0xBB67AE85u), B = (uint32_t)q ^ (k0 + 2u * 0x9E3779B9u);
+    const uint32_t C = (uint32_t)(r >> 32) ^ (k1 + 2u * 0xBB67AE85u), D = (uint32_t)r;
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(tab + 16u * (uint32_t)e), "r"(A), "r"(B), "r"(C), "r"(D)
+                 : "memory");
+  }
+}
+template <int NT, bool TAB = false>
 __device__ __forceinline__ void rand_words(uint32_t (&word)[NT], const uint64_t (&xp)[16], int w, int rq, uint32_t sg,
-                                           const RoundParams& p) {
+                                           const RoundParams& p, uint32_t tab = 0u) {
+  if constexpr (TAB) {                                              // the per-S* Philox table
+    const uint64_t q2 = (uint64_t)0xCD9E8D57u * sg;
+    const uint32_t x1 = (uint32_t)(q2 >> 32) ^ (uint32_t)rq ^ p.key0;
+    const uint64_t P = (uint64_t)0xD2511F53u * x1;
+    const uint32_t hP = (uint32_t)(P >> 32), lP = (uint32_t)P;
+    uint64_t X[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(X[k]) : "l"(xp[k]), "l"(0x4f8000004f800000ull));
+    auto pack4 = [&](uint32_t& acc, const uint4& o, int k0) {
+      uint64_t f23, f01, d23, d01;
+      asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+          : "=l"(f23) : "r"(o.z), "r"(o.w));
+      asm("{\n\t.reg .f32 a, b;\n\tcvt.rz.f32.u32 a, %1;\n\tcvt.rz.f32.u32 b, %2;\n\tmov.b64 %0, {a, b};\n\t}"
+          : "=l"(f01) : "r"(o.x), "r"(o.y));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d23) : "l"(f23), "l"(X[k0 + 1]));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d01) : "l"(f01), "l"(X[k0]));
+      acc = __funnelshift_l((uint32_t)(d23 >> 32), acc, 1);
+      acc = __funnelshift_l((uint32_t)d23, acc, 1);
+      acc = __funnelshift_l((uint32_t)(d01 >> 32), acc, 1);
+      acc = __funnelshift_l((uint32_t)d01, acc, 1);
+    };
+    auto start = [&](int q4, int j) {                               // the state after round 2
+      uint4 e;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                   : "r"(tab + 16u * (uint32_t)((8 * w + q4) * NT + j)));
+      const uint32_t z2 = hP ^ e.x;
+      const uint64_t p1 = (uint64_t)0xCD9E8D57u * z2;
+      return make_uint4((uint32_t)(p1 >> 32) ^ e.y, (uint32_t)p1, e.z ^ lP, e.w);
+    };
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      uint32_t hi = 0u, lo = 0u;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        uint4 o[2] = {start(q + 4, j), start(q, j)};
+        philox_tail_xk<2>(o, p.key0, p.key1);
+        pack4(hi, o[0], 2 * (q + 4));
+        pack4(lo, o[1], 2 * q);
+      }
+      word[j] = (hi << 16) | lo;
+    }
+    return;
+  }
   if constexpr (CM_RAND_CMP == 1) {
     uint32_t C[32];                                                 // ceil(x 2^32), saturated
 #pragma unroll
@@ -519,6 +616,8 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
   const uint32_t tiles = smem_u32(k1smem) + (uint32_t)(kSt * kStageBytes) * (uint32_t)wl;
   const uint32_t bars = smem_u32(k1smem + k1_bar_off(NT, false)) + 8u * (uint32_t)(kSt * wl);
   const uint32_t nibs = smem_u32(k1smem + k1_nib_off(NT, false));
+  const uint32_t rtabw = smem_u32(k1smem + k1_rtab_off(NT, p.nib32 ? p.nib_entries : 0, false)) +
+                         (uint32_t)p.rtab * (uint32_t)wl;
   const int G = p.G, n = p.n;
   const int64_t cs = p.cs;
   uint64_t tt[NT];                                                  // theta (-0 -> +0) in both halves
@@ -602,6 +701,11 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
     if (s >= p.s_count) break;
     uint32_t* out = hk.begin(s);
     const uint32_t sg = p.s0 + (uint32_t)(p.s_begin + s);           // RAND: global S* index
+    if constexpr (RAND && Hooks::kTab) {                            // this S*'s Philox table
+      __syncwarp();                                                 // the previous S*'s reads are done
+      rand_table_build(rtabw, Gr, NT, sg, p);
+      __syncwarp();
+    }
     for (int g = 0; g < Gr; ++g) {
       const int rq = 32 * g + lane + 1;                             // row owned by this lane
       // row masks (a1 reads i < t only, rows < n): FULL off the diagonal, nodes 32g .. rq-1 on it
@@ -622,7 +726,7 @@ __device__ __forceinline__ void k1_body_blk(const RoundParams& p, unsigned char*
       // consecutive blocks interleave in one basic block.
       auto pack = [&](const uint64_t (&xp)[16], uint32_t rmask, int w, uint32_t (&word)[NT]) {
         if (RAND) {
-          rand_words<NT>(word, xp, w, rq, sg, p);
+          rand_words<NT, RAND && Hooks::kTab>(word, xp, w, rq, sg, p, rtabw);
 #pragma unroll
           for (int j = 0; j < NT; ++j) word[j] &= rmask;
         } else {
@@ -1781,6 +1885,7 @@ __device__ __forceinline__ void warp_wait_geq(const uint32_t* p, uint32_t target
 }
 
 struct K1Ring {
+  static constexpr bool kTab = true;                              // randomized: the per-S* Philox table
   uint32_t* ring;
   int64_t slot_words;
   int32_t n_slots, n_theta, cs;
@@ -1847,8 +1952,9 @@ __host__ __device__ constexpr int fused_tmem_cols(int nt, bool rand) {   // per 
 }
 __host__ __device__ constexpr int fused_warps(int nt, bool rand) { return k1_warps(nt) + fused_scan_warps(nt, rand); }
 // dynamic shared memory: [K1 region, 1024-aligned][K2: graph blob, per-warp E / spill]
-__host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, bool bulk) {
-  return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 1023) & ~(size_t)1023;
+__host__ __device__ constexpr size_t fused_k1_bytes(int nt, int nib_entries, bool bulk, int rtab = 0) {
+  return (k1_nib_off(nt, bulk) + 4 * (size_t)nib_entries + 15) / 16 * 16 + (size_t)k1_warps(nt) * rtab + 1023 &
+         ~(size_t)1023;
 }
 
 // Register rebalance (setmaxnreg, whole warpgroups): more than 16 warps per CTA leave fewer than
@@ -1893,7 +1999,7 @@ __global__ void __launch_bounds__(32 * fused_warps(NT, RAND), CM_FUSED_MINB) fus
   extern __shared__ __align__(1024) unsigned char fraw[];
   unsigned char* base = fraw + ((1024u - (smem_u32(fraw) & 1023u)) & 1023u);
   unsigned char* k1smem = base;
-  unsigned char* k2smem = base + fused_k1_bytes(NT, fp.rp.nib32 ? fp.rp.nib_entries : 0, LAY == 1);
+  unsigned char* k2smem = base + fused_k1_bytes(NT, fp.rp.nib32 ? fp.rp.nib_entries : 0, LAY == 1, fp.rp.rtab);
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& sp = fp.sp;
